@@ -1,0 +1,140 @@
+/*
+ * fastid_b200.h -- C ABI of the B200-native FastID comparison path.
+ *
+ * Plain pointers and sizes only.  Every entry point returns a fastid_status;
+ * on failure fastid_last_error() holds a thread-local message.  Functions
+ * taking a `stream` accept a cudaStream_t passed as void* (NULL = default
+ * stream) and DEVICE pointers; they enqueue work and return without syncing.
+ * fastid_run_kernel takes HOST pointers and is synchronous.
+ *
+ * Reference interfaces each entry replaces (paths under the reference
+ * package pkg/src/fastid/):
+ *   fastid_run_kernel        run_naive_kernel        kernel.py:350-353
+ *                            run_blocked_kernel      kernel.py:317-347
+ *                            Executor.run seam       scheduler.py:221-240
+ *   fastid_compare_full      _naive_kernel / _blocked_worker kernel.py:224-269
+ *                            (behind compare_naive / compare_blocked kernel.py:283-314)
+ *   fastid_pack_bits         codec.pack              codec.py:118-127
+ *   fastid_pack_genotypes    codec.encode_genotype + pack codec.py:99-127
+ *   fastid_load_words        Panel words -> device rows (Panel kernel.py:68-129)
+ *   fastid_compare_topk      no reference equivalent; the
+ *   fastid_compare_threshold derivation of compare_naive's matrix, see DESIGN.md
+ *   fastid_merge_topk        multi-device combine (paper future work)
+ *
+ * Device row layout: every profile row occupies fastid_row_stride(L) bytes
+ * (a multiple of 16), holding the panel's words in their native little-endian
+ * byte order followed by zero fill.  Bit order inside a row does not affect the
+ * score as long as both operands share it, so u32 and u64 panels load as-is.
+ */
+#ifndef FASTID_B200_H
+#define FASTID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FASTID_API __attribute__((visibility("default")))
+#else
+#define FASTID_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FASTID_ABI_VERSION 1
+
+enum fastid_status {
+    FASTID_OK = 0,
+    FASTID_E_INVALID = 1,     /* bad argument (maps to ValueError)                */
+    FASTID_E_MISMATCH = 2,    /* incompatible panels (maps to PanelMismatchError) */
+    FASTID_E_CUDA = 3,        /* CUDA runtime/driver failure                      */
+    FASTID_E_CAPACITY = 4,    /* output buffer too small; count still reported    */
+    FASTID_E_NOMEM = 5,       /* device allocation failed                         */
+    FASTID_E_UNSUPPORTED = 6  /* formulation/shape not supported on this device   */
+};
+
+enum fastid_formulation {
+    FASTID_AUTO = 0,       /* the measured winner (tensor, mxf4)               */
+    FASTID_POPC = 1,       /* CUDA cores: LOP3 (and-not) + POPC over u32 words  */
+    FASTID_TENSOR_I8 = 2,  /* tcgen05.mma kind::i8 on 0/1-unpacked tiles        */
+    FASTID_TENSOR_F4 = 3   /* tcgen05.mma kind::mxf4 (e2m1 0/1, unit scales)    */
+};
+
+FASTID_API int fastid_abi_version(void);
+FASTID_API const char* fastid_last_error(void);
+/* bytes per device row for a panel of bit_length loci: ceil(L / 128) * 16 */
+FASTID_API int64_t fastid_row_stride(int64_t bit_length);
+/* largest k accepted by fastid_compare_topk */
+FASTID_API int fastid_max_k(void);
+/* 1 if `formulation` can run panels of bit_length loci on this build, else 0 */
+FASTID_API int fastid_supports(int formulation, int64_t bit_length);
+
+/* ---- profile encoder ---------------------------------------------------- */
+
+/* Copy `rows` panel rows of src_row_bytes each (u32/u64 words, little-endian)
+ * into the aligned device layout, zero-filling each row to dst_stride. */
+FASTID_API int fastid_load_words(const void* src, int64_t rows, int64_t src_row_bytes, void* dst,
+                      int64_t dst_stride, void* stream);
+
+/* Pack a (rows x bit_length) 0/1 byte matrix into MSB-first words of
+ * word_bits (32|64) exactly as codec.pack, written in the device layout. */
+FASTID_API int fastid_pack_bits(const uint8_t* bits, int64_t rows, int64_t bit_length, int word_bits,
+                     void* dst, int64_t dst_stride, void* stream);
+
+/* Encode (rows x n_loci) genotype codes (0=MM, 1=Mm, 2=mM, 3=mm) into
+ * 2*n_loci minor-allele bits (codec.GENOTYPE_BITS) and pack as above. */
+FASTID_API int fastid_pack_genotypes(const uint8_t* codes, int64_t rows, int64_t n_loci, int word_bits,
+                          void* dst, int64_t dst_stride, void* stream);
+
+/* ---- comparison --------------------------------------------------------- */
+
+/* out[i * ld_out + j] = popcount(refs_i AND NOT queries_j) for all i < n_refs,
+ * j < n_queries.  refs / queries are device rows of `stride` bytes. */
+FASTID_API int fastid_compare_full(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                        int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out,
+                        int formulation, void* stream);
+
+/* Workspace bytes fastid_compare_topk needs for this shape. */
+FASTID_API int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, int formulation,
+                          size_t* bytes);
+
+/* Per query j: the k (score, known index) pairs with the smallest scores,
+ * ordered by (score asc, index asc), restricted to score <= max_score.
+ * Outputs are [n_queries][k]; unused slots hold score 0xFFFFFFFF, index -1.
+ * Reported indices are ref_base + local row. */
+FASTID_API int fastid_compare_topk(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                        int64_t stride, int64_t bit_length, int k, uint32_t max_score,
+                        int64_t ref_base, uint32_t* top_scores, int64_t* top_index,
+                        void* workspace, size_t workspace_bytes, int formulation, void* stream);
+
+/* Every (query j, known i, score) with score <= threshold, in no particular
+ * order.  *hit_count (device) receives the total number of hits; only the first
+ * `capacity` are stored. */
+FASTID_API int fastid_compare_threshold(const void* refs, int64_t n_refs, const void* queries,
+                             int64_t n_queries, int64_t stride, int64_t bit_length,
+                             uint32_t threshold, int64_t ref_base, uint32_t* hit_query,
+                             int64_t* hit_ref, uint32_t* hit_score, int64_t capacity,
+                             unsigned long long* hit_count, int formulation, void* stream);
+
+/* Merge n_lists candidate lists, each [n_queries][k_in] sorted by (score, index),
+ * into the first k per query (lists laid out list-major). */
+FASTID_API int fastid_merge_topk(const uint32_t* cand_scores, const int64_t* cand_index, int n_lists,
+                      int64_t n_queries, int k_in, int k, uint32_t* top_scores,
+                      int64_t* top_index, void* stream);
+
+/* ---- host-buffer drop-in (synchronous) ----------------------------------- */
+
+/* Executor.run semantics: ref_words (n_refs x n_words), query_words
+ * (n_queries x n_words), or (n_words x n_queries) when queries_transposed,
+ * words of word_bits (32|64), out (n_refs x n_queries) u32, all HOST memory.
+ * Uses a per-thread device context on the current CUDA device. */
+FASTID_API int fastid_run_kernel(const void* ref_words, int64_t n_refs, const void* query_words,
+                      int64_t n_queries, int64_t n_words, int word_bits, int queries_transposed,
+                      uint32_t* out, int formulation);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTID_B200_H */

@@ -1,0 +1,395 @@
+"""Drop-in comparison entry points over the sm_100a library.
+
+Reference surface mirrored here (pkg/src/fastid/ in the reference):
+
+=============================  ==============================================
+reference                      this package
+=============================  ==============================================
+compare_naive(refs, queries)   compare_b200(refs, queries)     kernel.py:283
+compare_blocked(refs, layout,  compare_blocked_b200(...)       kernel.py:295
+  tile, parallelism)
+run_naive_kernel(r, q, out)    run_b200_kernel(r, q, out)      kernel.py:350
+run_blocked_kernel(r, qT, ..)  run_b200_kernel(r, qT, out,     kernel.py:317
+                                 queries_transposed=True)
+NaiveExecutor / Blocked...     B200Executor (run_pipeline seam) scheduler.py:221
+(none)            topk / threshold_hits (fused epilogues)
+=============================  ==============================================
+
+Validation happens here, before any native call, and raises the reference's
+exception types (``PanelMismatchError`` for bit-length/width mismatch,
+kernel.py:272-280; ``ValueError`` for parallelism < 1, kernel.py:308-309).
+Empty panels return empty results (kernel.py:289-291).
+
+PyTorch is used only for device memory and the current stream; every score
+is computed by the CUDA kernels in ``csrc/``.  There is no CPU fallback: if
+the library is missing or no GPU is present the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import CodecError, PanelMismatchError
+from .panel import Panel, QueryLayout, ScoreMatrix, ThresholdHits, TileConfig, TopKResult, word_dtype
+
+__all__ = [
+    "DevicePanel",
+    "B200Executor",
+    "compare_b200",
+    "compare_blocked_b200",
+    "compare_device",
+    "run_b200_kernel",
+    "topk",
+    "topk_device",
+    "threshold_hits",
+    "row_stride",
+]
+
+EMPTY_SCORE = 0xFFFFFFFF
+
+
+def row_stride(bit_length: int) -> int:
+    """Bytes per device row: ceil(L / 128) * 16 (16-B aligned rows)."""
+    return -(-bit_length // 128) * 16
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        from .errors import DeviceError
+
+        raise DeviceError("no CUDA device is visible; the B200 path has no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def _check_panels(ref_bits: int, ref_width: int, query_bits: int, query_width: int) -> None:
+    """Same conditions and messages as the reference's _check_panels (kernel.py:272-280)."""
+    if ref_bits != query_bits:
+        raise PanelMismatchError(f"panel bit lengths differ: refs {ref_bits}, queries {query_bits}")
+    if ref_width != query_width:
+        raise PanelMismatchError(f"panel word widths differ: refs {ref_width}, queries {query_width}")
+
+
+class DevicePanel:
+    """A panel resident in HBM in the aligned row layout.
+
+    ``rows`` is a uint8 tensor of shape (n_profiles, stride); row i holds the
+    profile's words in native little-endian order, zero filled to ``stride``.
+    This is how the known database stays resident between query batches.
+    """
+
+    def __init__(self, rows: torch.Tensor, bit_length: int, word_width: int, ids=None):
+        if rows.dtype != torch.uint8 or rows.dim() != 2 or not rows.is_cuda:
+            raise ValueError("rows must be a 2-D uint8 CUDA tensor")
+        if rows.shape[1] != row_stride(bit_length):
+            raise ValueError(f"row stride {rows.shape[1]} does not match {row_stride(bit_length)}")
+        if rows.data_ptr() % 16:
+            raise ValueError("rows must be 16-byte aligned")
+        self.rows = rows
+        self.bit_length = int(bit_length)
+        self.word_width = int(word_width)
+        self.ids = tuple(ids) if ids is not None else None
+
+    # -- construction (the profile encoder) --------------------------------
+    @classmethod
+    def empty(cls, n: int, bit_length: int, word_width: int = 64, device=None) -> "DevicePanel":
+        dev = _require_cuda(device)
+        return cls(torch.zeros((n, row_stride(bit_length)), dtype=torch.uint8, device=dev),
+                   bit_length, word_width)
+
+    @classmethod
+    def from_words(cls, words, bit_length: int, ids=None, device=None) -> "DevicePanel":
+        """Upload a (N, N_W) u32/u64 word array (host numpy or CUDA tensor)."""
+        dev = _require_cuda(device)
+        if isinstance(words, torch.Tensor):
+            if words.dtype not in (torch.int32, torch.int64, torch.uint32, torch.uint64):
+                raise ValueError("word tensors must be 32- or 64-bit integers")
+            width = words.element_size() * 8
+            src = words.to(dev).contiguous()
+            n, n_words = src.shape
+        else:
+            arr = np.ascontiguousarray(words)
+            if arr.dtype not in (np.uint32, np.uint64) or arr.ndim != 2:
+                raise ValueError("word arrays must be 2-D uint32/uint64")
+            width = arr.dtype.itemsize * 8
+            n, n_words = arr.shape
+            raw = arr.view(np.uint8).reshape(n, -1) if n else np.zeros((0, n_words * width // 8), np.uint8)
+            if not raw.flags.writeable:
+                raw = raw.copy()
+            src = torch.from_numpy(raw).to(dev)
+        out = cls.empty(n, bit_length, width, dev)
+        out.ids = tuple(ids) if ids is not None else None
+        if n:
+            with torch.cuda.device(dev):
+                _native.check(_native.lib().fastid_load_words(
+                    src.data_ptr(), n, n_words * width // 8, out.rows.data_ptr(), out.stride,
+                    _stream(dev)), "fastid_load_words")
+                torch.cuda.current_stream(dev).synchronize()  # src must outlive the copy
+        return out
+
+    @classmethod
+    def from_panel(cls, panel, device=None) -> "DevicePanel":
+        return cls.from_words(np.asarray(panel.words), panel.bit_length, getattr(panel, "ids", None), device)
+
+    @classmethod
+    def from_bits(cls, bits, word_width: int = 64, ids=None, device=None) -> "DevicePanel":
+        """Pack a (N, L) 0/1 byte matrix on the GPU exactly as codec.pack (codec.py:118-127)."""
+        word_dtype(word_width)
+        dev = _require_cuda(device)
+        t = bits if isinstance(bits, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(bits, np.uint8))
+        if t.dim() != 2 or t.dtype != torch.uint8:
+            raise CodecError("profile bits must be a 2-D uint8 matrix")
+        t = t.to(dev).contiguous()
+        n, length = t.shape
+        if length == 0:
+            raise CodecError("profile bits must be non-empty")
+        if n and int(t.max()) > 1:
+            raise CodecError("profile bits must contain only 0 and 1")
+        out = cls.empty(n, length, word_width, dev)
+        out.ids = tuple(ids) if ids is not None else None
+        if n:
+            with torch.cuda.device(dev):
+                _native.check(_native.lib().fastid_pack_bits(
+                    t.data_ptr(), n, length, word_width, out.rows.data_ptr(), out.stride, _stream(dev)),
+                    "fastid_pack_bits")
+        return out
+
+    @classmethod
+    def from_genotypes(cls, codes, word_width: int = 64, ids=None, device=None) -> "DevicePanel":
+        """Encode (N, loci) genotype codes 0=MM 1=Mm 2=mM 3=mm to 2 bits/locus (codec.py:99-115)."""
+        word_dtype(word_width)
+        dev = _require_cuda(device)
+        t = codes if isinstance(codes, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(codes, np.uint8))
+        if t.dim() != 2 or t.dtype != torch.uint8 or t.shape[1] == 0:
+            raise CodecError("genotype codes must be a non-empty 2-D uint8 matrix")
+        t = t.to(dev).contiguous()
+        n, loci = t.shape
+        if n and int(t.max()) > 3:
+            bad = int(torch.nonzero(t.reshape(-1) > 3)[0])
+            raise CodecError(f"unknown genotype code at position {bad % loci} of profile {bad // loci}")
+        out = cls.empty(n, 2 * loci, word_width, dev)
+        out.ids = tuple(ids) if ids is not None else None
+        if n:
+            with torch.cuda.device(dev):
+                _native.check(_native.lib().fastid_pack_genotypes(
+                    t.data_ptr(), n, loci, word_width, out.rows.data_ptr(), out.stride, _stream(dev)),
+                    "fastid_pack_genotypes")
+        return out
+
+    # -- views ---------------------------------------------------------------
+    @property
+    def n_profiles(self) -> int:
+        return int(self.rows.shape[0])
+
+    @property
+    def stride(self) -> int:
+        return int(self.rows.shape[1])
+
+    @property
+    def device(self) -> torch.device:
+        return self.rows.device
+
+    @property
+    def n_words(self) -> int:
+        return -(-self.bit_length // self.word_width)
+
+    def slice(self, start: int, stop: int) -> "DevicePanel":
+        ids = self.ids[start:stop] if self.ids is not None else None
+        return DevicePanel(self.rows[start:stop], self.bit_length, self.word_width, ids)
+
+    def to_words(self) -> np.ndarray:
+        """Download as a (N, N_W) word array (inverse of from_words)."""
+        nbytes = self.n_words * self.word_width // 8
+        host = self.rows[:, :nbytes].contiguous().cpu().numpy()
+        return host.view(word_dtype(self.word_width)).reshape(self.n_profiles, self.n_words)
+
+    def to_panel(self) -> Panel:
+        ids = self.ids if self.ids is not None else tuple(f"p{i}" for i in range(self.n_profiles))
+        return Panel(ids, self.to_words(), self.bit_length)
+
+
+def _as_device(p, device) -> DevicePanel:
+    if isinstance(p, DevicePanel):
+        return p
+    return DevicePanel.from_panel(p, device)
+
+
+def _ptr(p: DevicePanel) -> int:
+    return p.rows.data_ptr() if p.n_profiles else 0
+
+
+def compare_device(refs: DevicePanel, queries: DevicePanel, out: torch.Tensor | None = None,
+                   formulation: str | int = "auto") -> torch.Tensor:
+    """Full (N_R, N_Q) u32 score matrix on the device (int32 storage, reinterpret as u32)."""
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    dev = refs.device
+    if out is None:
+        out = torch.empty((refs.n_profiles, queries.n_profiles), dtype=torch.int32, device=dev)
+    if out.shape[0] != refs.n_profiles or out.shape[1] < queries.n_profiles or out.dtype != torch.int32:
+        raise ValueError("out must be an int32 tensor of shape (N_R, >= N_Q)")
+    if out.numel() and out.stride(1) != 1:
+        raise ValueError("out rows must be contiguous")
+    if refs.n_profiles and queries.n_profiles:
+        with torch.cuda.device(dev):
+            _native.check(_native.lib().fastid_compare_full(
+                _ptr(refs), refs.n_profiles, _ptr(queries), queries.n_profiles, refs.stride,
+                refs.bit_length, out.data_ptr(), out.stride(0), _native.formulation_code(formulation),
+                _stream(dev)), "fastid_compare_full")
+    return out
+
+
+def compare_b200(refs, queries, formulation: str | int = "auto", device=None) -> ScoreMatrix:
+    """``compare_naive`` on the B200 (kernel.py:283-292): same signature, errors and empties."""
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    n_r, n_q = refs.words.shape[0], queries.words.shape[0]
+    ref_ids = getattr(refs, "ids", tuple(f"r{i}" for i in range(n_r)))
+    q_ids = getattr(queries, "ids", tuple(f"q{j}" for j in range(n_q)))
+    if n_r == 0 or n_q == 0:
+        return ScoreMatrix(ref_ids, q_ids, np.zeros((n_r, n_q), dtype=np.uint32))
+    dev = _require_cuda(device)
+    d = compare_device(_as_device(refs, dev), _as_device(queries, dev), formulation=formulation)
+    scores = d.cpu().numpy().view(np.uint32)
+    return ScoreMatrix(ref_ids, q_ids, scores)
+
+
+def compare_blocked_b200(refs, queries: QueryLayout, tile: TileConfig | None = None, parallelism: int = 1,
+                         formulation: str | int = "auto", device=None) -> ScoreMatrix:
+    """``compare_blocked`` on the B200 (kernel.py:295-314).  ``tile`` and
+    ``parallelism`` are validated exactly as the reference does and otherwise
+    ignored: the device tiling is fixed by the kernel."""
+    tile = tile or TileConfig()
+    if parallelism < 1:
+        raise ValueError("parallelism must be at least 1")
+    from .panel import restore_queries
+
+    return compare_b200(refs, restore_queries(queries), formulation, device)
+
+
+def run_b200_kernel(ref_words: np.ndarray, query_words: np.ndarray, out: np.ndarray,
+                    queries_transposed: bool = False, formulation: str | int = "auto") -> None:
+    """Raw-array dispatch through the C ABI's host-buffer entry (fastid_run_kernel).
+
+    Matches run_naive_kernel (kernel.py:350-353) -- and run_blocked_kernel
+    (kernel.py:317-347) with ``queries_transposed=True`` -- writing every cell
+    of the caller-owned ``out`` (N_R, N_Q) u32 array.
+    """
+    ref_words = np.ascontiguousarray(ref_words)
+    query_words = np.ascontiguousarray(query_words)
+    if ref_words.dtype != query_words.dtype or ref_words.dtype not in (np.uint32, np.uint64):
+        raise PanelMismatchError(f"word dtypes differ or unsupported: {ref_words.dtype} vs {query_words.dtype}")
+    n_refs, n_words = ref_words.shape
+    n_q = query_words.shape[1] if queries_transposed else query_words.shape[0]
+    qw = query_words.shape[0] if queries_transposed else query_words.shape[1]
+    if qw != n_words:
+        raise PanelMismatchError(f"word counts differ: refs {n_words}, queries {qw}")
+    if out.shape != (n_refs, n_q) or out.dtype != np.uint32 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous uint32 array of shape {(n_refs, n_q)}")
+    if out.size == 0:
+        return
+    _require_cuda()
+    _native.check(_native.lib().fastid_run_kernel(
+        ref_words.ctypes.data, n_refs, query_words.ctypes.data, n_q, n_words, ref_words.dtype.itemsize * 8,
+        int(bool(queries_transposed)), out.ctypes.data, _native.formulation_code(formulation)),
+        "fastid_run_kernel")
+
+
+class B200Executor:
+    """Executor for the reference pipeline's seam (scheduler.py:221-246):
+    ``run_pipeline(plan, refs, queries, executor=B200Executor())``."""
+
+    wants_transposed = False
+
+    def __init__(self, formulation: str | int = "auto"):
+        self.formulation = formulation
+        self.calls = 0
+
+    def run(self, ref_words: np.ndarray, query_words: np.ndarray, out: np.ndarray) -> None:
+        self.calls += 1
+        run_b200_kernel(ref_words, query_words, out, queries_transposed=self.wants_transposed,
+                        formulation=self.formulation)
+
+
+def topk_workspace_bytes(n_refs: int, n_queries: int, k: int, formulation: str | int = "auto") -> int:
+    n = ctypes.c_size_t(0)
+    _native.check(_native.lib().fastid_topk_workspace(n_refs, n_queries, k, _native.formulation_code(formulation),
+                                                      ctypes.byref(n)), "fastid_topk_workspace")
+    return int(n.value)
+
+
+def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int | None = None,
+                ref_base: int = 0, formulation: str | int = "auto", workspace: torch.Tensor | None = None,
+                out: tuple | None = None):
+    """Fused compare + top-k on the device -> (scores int32 [N_Q, k] as u32, index int64 [N_Q, k])."""
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    max_k = _native.lib().fastid_max_k()
+    if not 1 <= k <= max_k:
+        raise ValueError(f"k must be in [1, {max_k}]")
+    dev = refs.device
+    n_q = queries.n_profiles
+    if out is None:
+        out = (torch.empty((n_q, k), dtype=torch.int32, device=dev),
+               torch.empty((n_q, k), dtype=torch.int64, device=dev))
+    s, x = out
+    need = topk_workspace_bytes(refs.n_profiles, n_q, k, formulation)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    ms = EMPTY_SCORE - 1 if max_score is None else int(max_score)
+    if n_q:
+        with torch.cuda.device(dev):
+            _native.check(_native.lib().fastid_compare_topk(
+                _ptr(refs), refs.n_profiles, _ptr(queries), n_q, refs.stride, refs.bit_length, k, ms, ref_base,
+                s.data_ptr(), x.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                _native.formulation_code(formulation), _stream(dev)), "fastid_compare_topk")
+    return s, x
+
+
+def topk(refs, queries, k: int, max_score: int | None = None, formulation: str | int = "auto",
+         device=None) -> TopKResult:
+    """Per unknown, the k closest knowns by (score asc, known index asc), optionally score <= max_score."""
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    dev = _require_cuda(device)
+    dr, dq = _as_device(refs, dev), _as_device(queries, dev)
+    s, x = topk_device(dr, dq, k, max_score, 0, formulation)
+    q_ids = getattr(queries, "ids", None) or tuple(f"q{j}" for j in range(dq.n_profiles))
+    return TopKResult(tuple(q_ids), s.cpu().numpy().view(np.uint32), x.cpu().numpy(),
+                      getattr(refs, "ids", None))
+
+
+def threshold_hits(refs, queries, threshold: int, capacity: int | None = None,
+                   formulation: str | int = "auto", device=None, ref_base: int = 0) -> ThresholdHits:
+    """Every (unknown j, known i, score) with score <= threshold, ordered by (j, i)."""
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    dev = _require_cuda(device)
+    dr, dq = _as_device(refs, dev), _as_device(queries, dev)
+    cap = int(capacity) if capacity is not None else max(1 << 16, 4 * dq.n_profiles)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    for _ in range(2):
+        hq = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        hr = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        hs = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            _native.check(_native.lib().fastid_compare_threshold(
+                _ptr(dr), dr.n_profiles, _ptr(dq), dq.n_profiles, dr.stride, dr.bit_length, int(threshold),
+                ref_base, hq.data_ptr(), hr.data_ptr(), hs.data_ptr(), cap, count.data_ptr(),
+                _native.formulation_code(formulation), _stream(dev)), "fastid_compare_threshold")
+        n = int(count.item())
+        if n <= cap:
+            break
+        cap = n  # second pass with an exact-size buffer
+    q = hq[:n].cpu().numpy().view(np.uint32)
+    r = hr[:n].cpu().numpy()
+    sc = hs[:n].cpu().numpy().view(np.uint32)
+    order = np.lexsort((r, q))
+    return ThresholdHits(q[order], r[order], sc[order], int(threshold))

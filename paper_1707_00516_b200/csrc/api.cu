@@ -1,0 +1,282 @@
+// C ABI entry points (include/fastid_b200.h): argument checks, formulation
+// dispatch, the top-k workspace protocol and the synchronous host-buffer
+// drop-in behind fastid_run_kernel.
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace fastid {
+
+namespace {
+thread_local std::string g_error;
+}
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+}
+
+const char* get_error() { return g_error.c_str(); }
+
+namespace {
+
+int list_size_for(int k) { return k <= 8 ? 8 : (k <= 16 ? 16 : 32); }
+
+int resolve_formulation(int formulation, int64_t bit_length) {
+    if (formulation == FASTID_AUTO) {
+        return tensor_supported(bit_length, FASTID_TENSOR_F4) ? FASTID_TENSOR_F4 : FASTID_POPC;
+    }
+    return formulation;
+}
+
+int check_compare(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries, int64_t stride,
+                  int64_t bit_length, int formulation) {
+    if (n_refs < 0 || n_queries < 0) FASTID_FAIL(FASTID_E_INVALID, "negative panel size");
+    if (bit_length <= 0) FASTID_FAIL(FASTID_E_INVALID, "bit_length must be positive");
+    if (stride < row_stride_bytes(bit_length) || stride % 16)
+        FASTID_FAIL(FASTID_E_INVALID, "stride %lld is not a multiple of 16 covering %lld bits", (long long)stride,
+                    (long long)bit_length);
+    if ((n_refs && ((uintptr_t)refs & 15)) || (n_queries && ((uintptr_t)queries & 15)))
+        FASTID_FAIL(FASTID_E_INVALID, "panel rows must be 16-byte aligned");
+    if (formulation < FASTID_AUTO || formulation > FASTID_TENSOR_F4)
+        FASTID_FAIL(FASTID_E_INVALID, "unknown formulation %d", formulation);
+    if (formulation >= FASTID_TENSOR_I8 && !tensor_supported(bit_length, formulation))
+        FASTID_FAIL(FASTID_E_UNSUPPORTED, "formulation %d does not support bit_length %lld", formulation,
+                    (long long)bit_length);
+    return FASTID_OK;
+}
+
+CompareArgs make_args(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries, int64_t stride,
+                      int64_t bit_length) {
+    CompareArgs a{};
+    a.refs = (const uint8_t*)refs;
+    a.queries = (const uint8_t*)queries;
+    a.n_refs = n_refs;
+    a.n_queries = n_queries;
+    a.stride = stride;
+    a.bit_length = bit_length;
+    return a;
+}
+
+int parts_for(int formulation, int64_t n_refs, int64_t n_queries) {
+    return formulation == FASTID_POPC ? popc_parts(n_refs, n_queries)
+                                      : tensor_parts(n_refs, n_queries, formulation);
+}
+
+int launch(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream) {
+    if (formulation == FASTID_POPC) return launch_popc(mode, a, n_parts, stream);
+    return launch_tensor(mode, a, formulation, n_parts, stream);
+}
+
+// ---- host-buffer context for fastid_run_kernel ------------------------------
+
+struct HostContext {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    void* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // staging, refs, queries, out
+    size_t cap[4] = {0, 0, 0, 0};
+
+    ~HostContext() {
+        for (void* p : buf)
+            if (p) cudaFree(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    int ensure(int slot, size_t bytes) {
+        if (bytes <= cap[slot]) return FASTID_OK;
+        if (buf[slot]) cudaFree(buf[slot]);
+        buf[slot] = nullptr;
+        cap[slot] = 0;
+        if (cudaMalloc(&buf[slot], bytes) != cudaSuccess) {
+            cudaGetLastError();
+            FASTID_FAIL(FASTID_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
+        }
+        cap[slot] = bytes;
+        return FASTID_OK;
+    }
+};
+
+thread_local HostContext* g_host_ctx = nullptr;
+
+int host_context(HostContext** out) {
+    int dev = 0;
+    FASTID_CUDA(cudaGetDevice(&dev));
+    if (g_host_ctx && g_host_ctx->device != dev) {
+        delete g_host_ctx;
+        g_host_ctx = nullptr;
+    }
+    if (!g_host_ctx) {
+        auto* c = new HostContext();
+        c->device = dev;
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            FASTID_FAIL(FASTID_E_CUDA, "cudaStreamCreate failed");
+        }
+        g_host_ctx = c;
+    }
+    *out = g_host_ctx;
+    return FASTID_OK;
+}
+
+__global__ void transpose_words_kernel(const uint8_t* __restrict__ src, int64_t n_words, int64_t n_cols,
+                                       int word_bytes, uint8_t* __restrict__ dst, int64_t dst_stride) {
+    // src is (n_words, n_cols) words; dst row c gets word w of column c.
+    const int64_t lanes_per_row = dst_stride / 4;
+    const int64_t total = n_cols * lanes_per_row;
+    const int64_t used = n_words * word_bytes / 4;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = t / lanes_per_row;
+        const int64_t l = t - c * lanes_per_row;
+        uint32_t v = 0;
+        if (l < used) {
+            const int64_t w = l * 4 / word_bytes;
+            const int64_t part = (l * 4) % word_bytes;
+            v = *reinterpret_cast<const uint32_t*>(src + (w * n_cols + c) * word_bytes + part);
+        }
+        reinterpret_cast<uint32_t*>(dst + c * dst_stride)[l] = v;
+    }
+}
+
+}  // namespace
+}  // namespace fastid
+
+using namespace fastid;
+
+extern "C" int fastid_abi_version(void) { return FASTID_ABI_VERSION; }
+extern "C" const char* fastid_last_error(void) { return get_error(); }
+extern "C" int64_t fastid_row_stride(int64_t bit_length) { return bit_length > 0 ? row_stride_bytes(bit_length) : 0; }
+extern "C" int fastid_max_k(void) { return kMaxTopK; }
+extern "C" int fastid_supports(int formulation, int64_t bit_length) {
+    if (bit_length <= 0) return 0;
+    if (formulation == FASTID_AUTO || formulation == FASTID_POPC) return 1;
+    return tensor_supported(bit_length, formulation) ? 1 : 0;
+}
+
+extern "C" int fastid_compare_full(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                   int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out,
+                                   int formulation, void* stream) {
+    if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
+    if (ld_out < n_queries) FASTID_FAIL(FASTID_E_INVALID, "ld_out smaller than n_queries");
+    if (n_refs == 0 || n_queries == 0) return FASTID_OK;
+    CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
+    a.out = out;
+    a.ld_out = ld_out;
+    int parts = 0;
+    return launch(kFull, a, resolve_formulation(formulation, bit_length), &parts, (cudaStream_t)stream);
+}
+
+extern "C" int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, int formulation, size_t* bytes) {
+    if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
+    if (!bytes) FASTID_FAIL(FASTID_E_INVALID, "bytes is NULL");
+    // formulation AUTO resolves against the shape only through bit_length; the
+    // workspace is sized for the larger of the two partitions.
+    const int kp = list_size_for(k);
+    int parts = popc_parts(n_refs, n_queries);
+    for (int f = FASTID_TENSOR_I8; f <= FASTID_TENSOR_F4; ++f) {
+        const int p = tensor_parts(n_refs, n_queries, f);
+        if (p > parts) parts = p;
+    }
+    (void)formulation;
+    *bytes = (size_t)parts * (size_t)n_queries * (size_t)kp * (sizeof(uint32_t) + sizeof(int64_t)) + 256;
+    return FASTID_OK;
+}
+
+extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                   int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
+                                   uint32_t* top_scores, int64_t* top_index, void* workspace,
+                                   size_t workspace_bytes, int formulation, void* stream) {
+    if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
+    if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
+    if (n_queries == 0) return FASTID_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_refs == 0) {
+        FASTID_CUDA(cudaMemsetAsync(top_scores, 0xFF, (size_t)n_queries * k * sizeof(uint32_t), st));
+        FASTID_CUDA(cudaMemsetAsync(top_index, 0xFF, (size_t)n_queries * k * sizeof(int64_t), st));
+        return FASTID_OK;
+    }
+    size_t need = 0;
+    if (int rc = fastid_topk_workspace(n_refs, n_queries, k, formulation, &need)) return rc;
+    if (workspace_bytes < need)
+        FASTID_FAIL(FASTID_E_CAPACITY, "workspace of %zu bytes is smaller than the %zu required", workspace_bytes,
+                    need);
+    const int f = resolve_formulation(formulation, bit_length);
+    const int kp = list_size_for(k);
+    const int parts = parts_for(f, n_refs, n_queries);
+    CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
+    a.k = k;
+    a.kpad = kp;
+    a.max_score = max_score;
+    a.ref_base = ref_base;
+    a.part_index = (int64_t*)(((uintptr_t)workspace + 15) & ~(uintptr_t)15);
+    a.part_scores = (uint32_t*)(a.part_index + (size_t)parts * n_queries * kp);
+    int launched_parts = 0;
+    if (int rc = launch(kTopK, a, f, &launched_parts, st)) return rc;
+    if (launched_parts != parts) FASTID_FAIL(FASTID_E_INVALID, "internal: partition mismatch");
+    return launch_merge(a.part_scores, a.part_index, parts, n_queries, kp, k, top_scores, top_index, st);
+}
+
+extern "C" int fastid_compare_threshold(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                        int64_t stride, int64_t bit_length, uint32_t threshold, int64_t ref_base,
+                                        uint32_t* hit_query, int64_t* hit_ref, uint32_t* hit_score,
+                                        int64_t capacity, unsigned long long* hit_count, int formulation,
+                                        void* stream) {
+    if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
+    if (capacity < 0 || !hit_count) FASTID_FAIL(FASTID_E_INVALID, "bad hit buffers");
+    cudaStream_t st = (cudaStream_t)stream;
+    FASTID_CUDA(cudaMemsetAsync(hit_count, 0, sizeof(unsigned long long), st));
+    if (n_refs == 0 || n_queries == 0) return FASTID_OK;
+    CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
+    a.threshold = threshold;
+    a.ref_base = ref_base;
+    a.hit_query = hit_query;
+    a.hit_ref = hit_ref;
+    a.hit_score = hit_score;
+    a.capacity = capacity;
+    a.hit_count = hit_count;
+    int parts = 0;
+    return launch(kThreshold, a, resolve_formulation(formulation, bit_length), &parts, st);
+}
+
+extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries,
+                                 int64_t n_words, int word_bits, int queries_transposed, uint32_t* out,
+                                 int formulation) {
+    if (word_bits != 32 && word_bits != 64) FASTID_FAIL(FASTID_E_INVALID, "word_bits must be 32 or 64");
+    if (n_words <= 0 || n_refs < 0 || n_queries < 0) FASTID_FAIL(FASTID_E_INVALID, "bad panel shape");
+    if (n_refs == 0 || n_queries == 0) return FASTID_OK;
+    HostContext* ctx = nullptr;
+    if (int rc = host_context(&ctx)) return rc;
+    const int wb = word_bits / 8;
+    const int64_t row_bytes = n_words * wb;
+    const int64_t bit_length = n_words * word_bits;
+    const int64_t stride = row_stride_bytes(bit_length);
+    const size_t ref_in = (size_t)n_refs * row_bytes, q_in = (size_t)n_queries * row_bytes;
+    const size_t out_bytes = (size_t)n_refs * n_queries * 4;
+    if (int rc = ctx->ensure(0, ref_in > q_in ? ref_in : q_in)) return rc;
+    if (int rc = ctx->ensure(1, (size_t)n_refs * stride)) return rc;
+    if (int rc = ctx->ensure(2, (size_t)n_queries * stride)) return rc;
+    if (int rc = ctx->ensure(3, out_bytes)) return rc;
+    cudaStream_t st = ctx->stream;
+    // queries first (the staging buffer is reused for the refs)
+    FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], query_words, q_in, cudaMemcpyHostToDevice, st));
+    if (queries_transposed) {
+        const int64_t work = n_queries * (stride / 4);
+        transpose_words_kernel<<<(unsigned)(work < 148 * 64 * 32 ? ceil_div(work, 256) : 148 * 32), 256, 0, st>>>(
+            (const uint8_t*)ctx->buf[0], n_words, n_queries, wb, (uint8_t*)ctx->buf[2], stride);
+        FASTID_LAUNCHED("transpose_words_kernel");
+    } else if (int rc = fastid_load_words(ctx->buf[0], n_queries, row_bytes, ctx->buf[2], stride, st)) {
+        return rc;
+    }
+    FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], ref_words, ref_in, cudaMemcpyHostToDevice, st));
+    if (int rc = fastid_load_words(ctx->buf[0], n_refs, row_bytes, ctx->buf[1], stride, st)) return rc;
+    if (int rc = fastid_compare_full(ctx->buf[1], n_refs, ctx->buf[2], n_queries, stride, bit_length,
+                                     (uint32_t*)ctx->buf[3], n_queries, formulation, st))
+        return rc;
+    FASTID_CUDA(cudaMemcpyAsync(out, ctx->buf[3], out_bytes, cudaMemcpyDeviceToHost, st));
+    FASTID_CUDA(cudaStreamSynchronize(st));
+    return FASTID_OK;
+}

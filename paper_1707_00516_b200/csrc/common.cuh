@@ -1,0 +1,159 @@
+// Shared helpers for the FastID sm_100a library: status plumbing, launch
+// checks and the register-resident top-k list used by every epilogue.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "fastid_b200.h"
+
+namespace fastid {
+
+// Thread-local error message behind fastid_last_error().
+void set_error(const char* fmt, ...);
+const char* get_error();
+
+#define FASTID_FAIL(code, ...)                 \
+    do {                                       \
+        ::fastid::set_error(__VA_ARGS__);      \
+        return (code);                         \
+    } while (0)
+
+#define FASTID_CUDA(expr)                                                                     \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            FASTID_FAIL(FASTID_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                                  \
+    } while (0)
+
+#define FASTID_LAUNCHED(name)                                                                   \
+    do {                                                                                        \
+        cudaError_t _e = cudaGetLastError();                                                    \
+        if (_e != cudaSuccess)                                                                  \
+            FASTID_FAIL(FASTID_E_CUDA, "launch of %s failed: %s", name, cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr int kMaxTopK = 32;
+constexpr uint32_t kEmptyScore = 0xFFFFFFFFu;
+constexpr uint32_t kEmptyLocal = 0xFFFFFFFFu;
+
+inline int64_t row_stride_bytes(int64_t bit_length) { return ((bit_length + 127) / 128) * 16; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// (score, index) lexicographic order: the canonical tie-break of every top-k
+// output (score ascending, then known index ascending).
+__device__ __forceinline__ bool before(uint32_t s0, uint32_t i0, uint32_t s1, uint32_t i1) {
+    return s0 < s1 || (s0 == s1 && i0 < i1);
+}
+
+// A sorted list of K (score, local index) pairs held in registers.  Offers are
+// rare after warm-up (a candidate must beat the current K-th entry), so the
+// unrolled bubble insertion costs little; all indexing is static.
+template <int K>
+struct TopList {
+    uint32_t s[K];
+    uint32_t x[K];
+
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            s[i] = kEmptyScore;
+            x[i] = kEmptyLocal;
+        }
+    }
+    __device__ __forceinline__ bool admits(uint32_t v, uint32_t idx) const {
+        return before(v, idx, s[K - 1], x[K - 1]);
+    }
+    __device__ __forceinline__ void insert(uint32_t v, uint32_t idx) {
+        s[K - 1] = v;
+        x[K - 1] = idx;
+#pragma unroll
+        for (int p = K - 1; p > 0; --p) {
+            const bool sw = before(s[p], x[p], s[p - 1], x[p - 1]);
+            const uint32_t ts = sw ? s[p - 1] : s[p];
+            const uint32_t tx = sw ? x[p - 1] : x[p];
+            s[p - 1] = sw ? s[p] : s[p - 1];
+            x[p - 1] = sw ? x[p] : x[p - 1];
+            s[p] = ts;
+            x[p] = tx;
+        }
+    }
+    __device__ __forceinline__ void offer(uint32_t v, uint32_t idx, uint32_t max_score) {
+        if (v <= max_score && admits(v, idx)) insert(v, idx);
+    }
+    // Write the list as one partial candidate list: scores / global indices.
+    __device__ __forceinline__ void store(uint32_t* scores, int64_t* index, int64_t base) const {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            scores[i] = s[i];
+            index[i] = s[i] == kEmptyScore ? -1 : base + (int64_t)x[i];
+        }
+    }
+};
+
+// Kernel-side description of one comparison job (device rows of `stride` bytes).
+struct CompareArgs {
+    const uint8_t* refs;
+    const uint8_t* queries;
+    int64_t n_refs;
+    int64_t n_queries;
+    int64_t stride;      // bytes per row, multiple of 16
+    int64_t bit_length;
+    // full matrix
+    uint32_t* out;
+    int64_t ld_out;
+    // top-k
+    int k;
+    uint32_t max_score;
+    uint32_t* part_scores;  // [n_parts][n_queries][kpad]
+    int64_t* part_index;
+    int kpad;
+    // threshold
+    uint32_t threshold;
+    int64_t ref_base;
+    uint32_t* hit_query;
+    int64_t* hit_ref;
+    uint32_t* hit_score;
+    int64_t capacity;
+    unsigned long long* hit_count;
+};
+
+enum Mode { kFull = 0, kTopK = 1, kThreshold = 2 };
+
+// Append one threshold hit with a warp-aggregated slot reservation.
+__device__ __forceinline__ void emit_hits(const CompareArgs& a, bool hit, uint32_t q, int64_t r,
+                                          uint32_t v) {
+    const unsigned mask = __activemask();
+    const unsigned ballot = __ballot_sync(mask, hit);
+    if (!ballot) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(ballot) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(a.hit_count, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(mask, base, leader);
+    if (hit) {
+        const unsigned long long slot = base + __popc(ballot & ((1u << lane) - 1u));
+        if ((long long)slot < a.capacity) {
+            a.hit_query[slot] = q;
+            a.hit_ref[slot] = a.ref_base + r;
+            a.hit_score[slot] = v;
+        }
+    }
+}
+
+// Host-side launchers implemented per formulation.
+int launch_popc(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t stream);
+int popc_parts(int64_t n_refs, int64_t n_queries);
+int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream);
+int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation);
+int tensor_supported(int64_t bit_length, int formulation);
+int launch_merge(const uint32_t* cand_scores, const int64_t* cand_index, int n_lists,
+                 int64_t n_queries, int k_in, int k, uint32_t* top_scores, int64_t* top_index,
+                 cudaStream_t stream);
+
+}  // namespace fastid

@@ -1,0 +1,98 @@
+// Top-k combine: n_lists sorted candidate lists per query -> the first k by
+// (score asc, known index asc).  Used twice: to fold the per-CTA partial
+// lists of one device, and to fold the per-GPU lists after the NCCL gather
+// (the multi-GPU driver's only exchange).
+//
+// One warp per query: lane l owns lists l, l+32, ... (up to 16 per lane, so
+// n_lists <= 512); each of the k rounds takes the warp-wide minimum head and
+// advances the winning list.
+#include "common.cuh"
+
+namespace fastid {
+namespace {
+
+constexpr int kMaxListsPerLane = 16;
+
+__device__ __forceinline__ bool key_before(uint32_t s0, uint64_t i0, uint32_t s1, uint64_t i1) {
+    return s0 < s1 || (s0 == s1 && i0 < i1);
+}
+
+__global__ void merge_kernel(const uint32_t* __restrict__ cs, const int64_t* __restrict__ ci, int n_lists,
+                             int64_t n_queries, int k_in, int k, uint32_t* __restrict__ out_s,
+                             int64_t* __restrict__ out_i) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (q >= n_queries) return;
+    int head[kMaxListsPerLane];
+#pragma unroll
+    for (int m = 0; m < kMaxListsPerLane; ++m) head[m] = 0;
+
+    for (int o = 0; o < k; ++o) {
+        // best head among this lane's lists
+        uint32_t bs = kEmptyScore;
+        uint64_t bi = ~0ull;
+        int bm = -1;
+#pragma unroll
+        for (int m = 0; m < kMaxListsPerLane; ++m) {
+            const int l = lane + 32 * m;
+            if (l < n_lists && head[m] < k_in) {
+                const int64_t off = ((int64_t)l * n_queries + q) * k_in + head[m];
+                const uint32_t s = cs[off];
+                const uint64_t i = (uint64_t)ci[off];
+                if (s != kEmptyScore && key_before(s, i, bs, bi)) {
+                    bs = s;
+                    bi = i;
+                    bm = m;
+                }
+            }
+        }
+        // warp arg-min over (score, index); ties on the full key cannot occur
+        // between distinct lists because indices are unique
+        uint32_t ws = bs;
+        uint64_t wi = bi;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const uint32_t os = __shfl_xor_sync(0xffffffffu, ws, d);
+            const uint64_t oi = __shfl_xor_sync(0xffffffffu, wi, d);
+            if (key_before(os, oi, ws, wi)) {
+                ws = os;
+                wi = oi;
+            }
+        }
+        if (bm >= 0 && bs == ws && bi == wi) {
+#pragma unroll
+            for (int m = 0; m < kMaxListsPerLane; ++m)
+                if (m == bm) ++head[m];
+        }
+        if (lane == 0) {
+            out_s[q * k + o] = ws;
+            out_i[q * k + o] = ws == kEmptyScore ? -1 : (int64_t)wi;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_merge(const uint32_t* cs, const int64_t* ci, int n_lists, int64_t n_queries, int k_in, int k,
+                 uint32_t* out_s, int64_t* out_i, cudaStream_t stream) {
+    if (n_lists < 1 || n_lists > 32 * kMaxListsPerLane)
+        FASTID_FAIL(FASTID_E_INVALID, "n_lists must be in [1, %d], got %d", 32 * kMaxListsPerLane, n_lists);
+    if (k < 1 || k_in < 1) FASTID_FAIL(FASTID_E_INVALID, "k must be positive");
+    if (n_queries == 0) return FASTID_OK;
+    const int64_t threads = n_queries * 32;
+    const int block = 256;
+    merge_kernel<<<(unsigned)ceil_div(threads, block), block, 0, stream>>>(cs, ci, n_lists, n_queries, k_in, k,
+                                                                           out_s, out_i);
+    FASTID_LAUNCHED("merge_kernel");
+    return FASTID_OK;
+}
+
+}  // namespace fastid
+
+extern "C" int fastid_merge_topk(const uint32_t* cand_scores, const int64_t* cand_index, int n_lists,
+                                 int64_t n_queries, int k_in, int k, uint32_t* top_scores, int64_t* top_index,
+                                 void* stream) {
+    if (k > k_in) FASTID_FAIL(FASTID_E_INVALID, "k (%d) exceeds the candidate list length (%d)", k, k_in);
+    return fastid::launch_merge(cand_scores, cand_index, n_lists, n_queries, k_in, k, top_scores, top_index,
+                                (cudaStream_t)stream);
+}

@@ -1,0 +1,193 @@
+"""Parity of the sm_100a kernels with the oracle and the reference goldens.
+
+Every test here calls through the C ABI (include/fastid_b200.h) via the
+package; the oracle (oracle/) is only the checker.  Bar: bit-exact.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+
+from conftest import GOLDEN, gpu_available, rand_words
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+FORMS = ["popc", "tensor_i8", "tensor_f4", "auto"]
+
+
+def fb():
+    import paper_1707_00516_b200 as m
+
+    return m
+
+
+def _supported(form, L):
+    from paper_1707_00516_b200 import _native
+
+    return _native.supports(form, L)
+
+
+def panels(c):
+    m = fb()
+    L = c["bits"]
+    r = m.Panel(tuple(f"r{i}" for i in range(c["refs"].shape[0])), c["refs"], L)
+    q = m.Panel(tuple(f"q{j}" for j in range(c["queries"].shape[0])), c["queries"], L)
+    return r, q
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_full_matrix_goldens(kernel_cases, form):
+    for c in kernel_cases:
+        if not _supported(form, c["bits"]):
+            continue
+        r, q = panels(c)
+        got = fb().compare_b200(r, q, formulation=form)
+        assert got.scores.dtype == np.uint32
+        assert np.array_equal(got.scores, c["scores"]), (form, c["name"])
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_topk_goldens(topk_cases, form):
+    for c in topk_cases:
+        if not _supported(form, c["bits"]):
+            continue
+        r, q = panels(c)
+        k = int(c["k"])
+        res = fb().topk(r, q, k, formulation=form)
+        assert np.array_equal(res.scores, c["top_scores"]), (form, c["name"])
+        assert np.array_equal(res.index, c["top_index"]), (form, c["name"])
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_threshold_goldens(topk_cases, form):
+    for c in topk_cases:
+        if not _supported(form, c["bits"]):
+            continue
+        r, q = panels(c)
+        hits = fb().threshold_hits(r, q, int(c["threshold"]), formulation=form)
+        assert np.array_equal(hits.query, c["hit_query"]), (form, c["name"])
+        assert np.array_equal(hits.ref, c["hit_ref"]), (form, c["name"])
+        assert np.array_equal(hits.score, c["hit_score"]), (form, c["name"])
+
+
+@pytest.mark.parametrize("form", FORMS)
+@pytest.mark.parametrize("k", [1, 5, 16, 32])
+def test_topk_vs_oracle_random(rng, form, k):
+    for n_r, n_q, L, width in ((3000, 200, 1024, 64), (999, 129, 777, 32), (5, 300, 5000, 64)):
+        if not _supported(form, L):
+            continue
+        nw = -(-L // width)
+        r, _ = rand_words(rng, n_r, nw, width, L)
+        q, _ = rand_words(rng, n_q, nw, width, L)
+        # plant exact copies and duplicates so ties and zeros occur
+        q[: min(20, n_q)] = r[rng.integers(0, n_r, min(20, n_q))]
+        r[n_r // 2 : n_r // 2 + 3] = r[:3]
+        m = fb()
+        R, Q = m.Panel(tuple(range(n_r)), r, L), m.Panel(tuple(range(n_q)), q, L)
+        full = oracle.naive(r, q)
+        for ms in (None, int(np.percentile(full, 2))):
+            res = m.topk(R, Q, k, max_score=ms, formulation=form)
+            es, ex, _ = oracle.topk_from_matrix(full, k, 0xFFFFFFFE if ms is None else ms)
+            assert np.array_equal(res.scores, es), (form, n_r, n_q, L, ms)
+            assert np.array_equal(res.index, ex), (form, n_r, n_q, L, ms)
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_checksums_vs_reference(checksum_rows, form):
+    m = fb()
+    import torch
+
+    for row in checksum_rows:
+        refs = oracle.synth_words(row["n_refs"], row["n_words"], row["word_width"], row["seed"], 0)
+        queries = oracle.synth_words(row["n_queries"], row["n_words"], row["word_width"], row["seed"], 1)
+        L = row["n_words"] * row["word_width"]
+        if not _supported(form, L):
+            continue
+        dr = m.DevicePanel.from_words(refs, L)
+        dq = m.DevicePanel.from_words(queries, L)
+        out = m.compare_device(dr, dq, formulation=form)
+        scores = out.cpu().numpy().view(np.uint32)
+        assert oracle.score_checksum(scores) == row["checksum"], (form, row["label"])
+        del out
+        torch.cuda.empty_cache()
+
+
+def test_empty_panels():
+    m = fb()
+    r = m.Panel((), np.zeros((0, 2), np.uint64), 128)
+    q = m.Panel(("a", "b", "c"), np.zeros((3, 2), np.uint64), 128)
+    assert m.compare_b200(r, q).shape == (0, 3)
+    assert m.compare_b200(q, r).shape == (3, 0)
+    res = m.topk(r, q, 4)
+    assert (res.index == -1).all() and (res.scores == 0xFFFFFFFF).all()
+
+
+def test_mismatch_errors():
+    m = fb()
+    a = m.Panel(("a",), np.zeros((1, 2), np.uint32), 64)
+    b = m.Panel(("b",), np.zeros((1, 2), np.uint32), 40)
+    with pytest.raises(m.PanelMismatchError):
+        m.compare_b200(a, b)
+    c = m.Panel(("c",), np.zeros((1, 1), np.uint64), 64)
+    with pytest.raises(m.PanelMismatchError):
+        m.compare_b200(a, c)
+    with pytest.raises(ValueError):
+        m.compare_blocked_b200(a, m.relayout_queries(a), m.TileConfig(16), 0)
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_run_kernel_host_path(rng, form):
+    m = fb()
+    for width, transposed in ((64, False), (32, True)):
+        r, _ = rand_words(rng, 333, 1024 // width, width)
+        q, _ = rand_words(rng, 77, 1024 // width, width)
+        out = np.empty((333, 77), np.uint32)
+        qa = np.ascontiguousarray(q.T) if transposed else q
+        m.run_b200_kernel(r, qa, out, queries_transposed=transposed, formulation=form)
+        assert np.array_equal(out, oracle.naive(r, q))
+
+
+def test_executor_seam(rng):
+    m = fb()
+    r, _ = rand_words(rng, 100, 4, 64)
+    q, _ = rand_words(rng, 9, 4, 64)
+    ex = m.B200Executor()
+    out = np.empty((100, 9), np.uint32)
+    ex.run(r, q, out)
+    assert ex.calls == 1 and np.array_equal(out, oracle.naive(r, q))
+
+
+def test_encoder_matches_reference_pack(pack_cases):
+    m = fb()
+    for L in pack_cases["lengths"]:
+        bits = pack_cases[f"L{L}_bits"]
+        for width in (32, 64):
+            d = m.DevicePanel.from_bits(bits, width)
+            assert np.array_equal(d.to_words(), pack_cases[f"L{L}_w{width}"]), (L, width)
+            # padding of the device row is zero past the packed words
+            nb = d.n_words * width // 8
+            assert int(d.rows[:, nb:].sum()) == 0
+
+
+def test_genotype_encoder(genotype_rows):
+    m = fb()
+    codes_of = {"MM": 0, "Mm": 1, "mM": 2, "mm": 3}
+    for row in genotype_rows:
+        codes = np.array([[codes_of[c] for c in row["codes"]]], np.uint8)
+        d = m.DevicePanel.from_genotypes(codes, 32)
+        assert d.bit_length == len(row["bits"])
+        assert d.to_words().tolist() == [row["w32"]]
+    with pytest.raises(m.CodecError):
+        m.DevicePanel.from_genotypes(np.array([[0, 4]], np.uint8))
+
+
+def test_load_words_roundtrip(rng):
+    m = fb()
+    for width, L in ((32, 50), (64, 5000), (64, 1)):
+        w, _ = rand_words(rng, 17, -(-L // width), width, L)
+        d = m.DevicePanel.from_words(w, L)
+        assert d.stride % 16 == 0 and d.stride == m.row_stride(L)
+        assert np.array_equal(d.to_words(), w)
