@@ -108,6 +108,16 @@ FASTID_API int fastid_compare_topk(const void* refs, int64_t n_refs, const void*
                         int64_t ref_base, uint32_t* top_scores, int64_t* top_index,
                         void* workspace, size_t workspace_bytes, int formulation, void* stream);
 
+/* The first half of fastid_compare_topk: only the comparison kernel, leaving
+ * *n_lists candidate lists of *list_len entries per query in the workspace
+ * (indices at *index_offset, scores at *score_offset bytes from workspace,
+ * list-major [n_lists][n_queries][list_len]) for fastid_merge_topk. */
+FASTID_API int fastid_topk_partials(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                    int64_t stride, int64_t bit_length, int k, uint32_t max_score,
+                                    int64_t ref_base, void* workspace, size_t workspace_bytes,
+                                    int formulation, void* stream, int* n_lists, int* list_len,
+                                    size_t* index_offset, size_t* score_offset);
+
 /* Every (query j, known i, score) with score <= threshold, in no particular
  * order.  *hit_count (device) receives the total number of hits; only the first
  * `capacity` are stored. */
@@ -132,6 +142,15 @@ FASTID_API int fastid_merge_topk(const uint32_t* cand_scores, const int64_t* can
 FASTID_API int fastid_run_kernel(const void* ref_words, int64_t n_refs, const void* query_words,
                       int64_t n_queries, int64_t n_words, int word_bits, int queries_transposed,
                       uint32_t* out, int formulation);
+
+/* ---- measurement ------------------------------------------------------- */
+
+/* Pipe-peak probe (roofline denominator): launches an MMA-only (tensor
+ * formulations) or LOP3+POPC-only (FASTID_POPC) kernel, one CTA per SM, with
+ * `iters` inner iterations; *work receives the bit-pairs it performs.  Time it
+ * with CUDA events on `stream`.  `scratch` is >= 4 * SM-count bytes of device
+ * memory. */
+FASTID_API int fastid_probe_peak(int formulation, int iters, void* scratch, double* work, void* stream);
 
 #ifdef __cplusplus
 }

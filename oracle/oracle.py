@@ -212,3 +212,19 @@ def mask_padding(words: np.ndarray, bit_length: int) -> np.ndarray:
         keep = ((1 << width) - 1) ^ ((1 << (width - tail)) - 1)
         words[:, -1] &= words.dtype.type(keep)
     return words
+
+
+def merge_lists(scores: np.ndarray, index: np.ndarray, k: int):
+    """Merge [lists, N_Q, k_in] candidate lists into the first k per query by (score, index)."""
+    n_lists, n_q, k_in = scores.shape
+    s_out = np.full((n_q, k), 0xFFFFFFFF, dtype=np.uint32)
+    x_out = np.full((n_q, k), -1, dtype=np.int64)
+    for j in range(n_q):
+        s = scores[:, j, :].reshape(-1)
+        x = index[:, j, :].reshape(-1)
+        keep = x >= 0
+        s, x = s[keep], x[keep]
+        order = np.lexsort((x, s))[:k]
+        s_out[j, : len(order)] = s[order]
+        x_out[j, : len(order)] = x[order]
+    return s_out, x_out

@@ -22,7 +22,7 @@ REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 INCLUDE = REPO_DIR / "include"
 LIB_PATH = PKG_DIR / "_fastid_b200.so"
-SOURCES = ("api.cu", "encode.cu", "popc.cu", "tensor.cu", "merge.cu")
+SOURCES = ("api.cu", "encode.cu", "popc.cu", "tensor.cu", "merge.cu", "probe.cu")
 HEADERS = ("common.cuh", "tensor_ptx.cuh")
 
 NVCC_FLAGS = (
@@ -94,9 +94,13 @@ def lib() -> ctypes.CDLL:
             "fastid_compare_full": ([vp, i64, vp, i64, i64, i64, vp, i64, i32, vp], i32),
             "fastid_topk_workspace": ([i64, i64, i32, i32, ctypes.POINTER(sz)], i32),
             "fastid_compare_topk": ([vp, i64, vp, i64, i64, i64, i32, u32, i64, vp, vp, vp, sz, i32, vp], i32),
+            "fastid_topk_partials": ([vp, i64, vp, i64, i64, i64, i32, u32, i64, vp, sz, i32, vp,
+                                      ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(sz),
+                                      ctypes.POINTER(sz)], i32),
             "fastid_compare_threshold": ([vp, i64, vp, i64, i64, i64, u32, i64, vp, vp, vp, i64, vp, i32, vp], i32),
             "fastid_merge_topk": ([vp, vp, i32, i64, i32, i32, vp, vp, vp], i32),
             "fastid_run_kernel": ([vp, i64, vp, i64, i64, i32, i32, vp, i32], i32),
+            "fastid_probe_peak": ([i32, i32, vp, ctypes.POINTER(ctypes.c_double), vp], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

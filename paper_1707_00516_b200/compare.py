@@ -330,10 +330,16 @@ def topk_workspace_bytes(n_refs: int, n_queries: int, k: int, formulation: str |
 
 def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int | None = None,
                 ref_base: int = 0, formulation: str | int = "auto", workspace: torch.Tensor | None = None,
-                out: tuple | None = None):
-    """Fused compare + top-k on the device -> (scores int32 [N_Q, k] as u32, index int64 [N_Q, k])."""
+                out: tuple | None = None, events: tuple | None = None):
+    """Fused compare + top-k on the device -> (scores int32 [N_Q, k] as u32, index int64 [N_Q, k]).
+
+    Two launches on the current stream: the comparison kernel (writing
+    per-CTA candidate lists) and the merge kernel.  ``events=(start, end)``
+    are recorded around the comparison kernel alone (roofline timing).
+    """
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
-    max_k = _native.lib().fastid_max_k()
+    L = _native.lib()
+    max_k = L.fastid_max_k()
     if not 1 <= k <= max_k:
         raise ValueError(f"k must be in [1, {max_k}]")
     dev = refs.device
@@ -342,16 +348,31 @@ def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int 
         out = (torch.empty((n_q, k), dtype=torch.int32, device=dev),
                torch.empty((n_q, k), dtype=torch.int64, device=dev))
     s, x = out
+    if n_q == 0:
+        return s, x
+    ms = EMPTY_SCORE - 1 if max_score is None else int(max_score)
+    if refs.n_profiles == 0:
+        s.fill_(-1)
+        x.fill_(-1)
+        return s, x
     need = topk_workspace_bytes(refs.n_profiles, n_q, k, formulation)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
-    ms = EMPTY_SCORE - 1 if max_score is None else int(max_score)
-    if n_q:
-        with torch.cuda.device(dev):
-            _native.check(_native.lib().fastid_compare_topk(
-                _ptr(refs), refs.n_profiles, _ptr(queries), n_q, refs.stride, refs.bit_length, k, ms, ref_base,
-                s.data_ptr(), x.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                _native.formulation_code(formulation), _stream(dev)), "fastid_compare_topk")
+    lists, kp = ctypes.c_int(0), ctypes.c_int(0)
+    xo, so = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        if events is not None:
+            events[0].record(stream)
+        _native.check(L.fastid_topk_partials(
+            _ptr(refs), refs.n_profiles, _ptr(queries), n_q, refs.stride, refs.bit_length, k, ms, ref_base,
+            workspace.data_ptr(), workspace.numel(), _native.formulation_code(formulation), stream.cuda_stream,
+            ctypes.byref(lists), ctypes.byref(kp), ctypes.byref(xo), ctypes.byref(so)), "fastid_topk_partials")
+        if events is not None:
+            events[1].record(stream)
+        base = workspace.data_ptr()
+        _native.check(L.fastid_merge_topk(base + so.value, base + xo.value, lists.value, n_q, kp.value, k,
+                                          s.data_ptr(), x.data_ptr(), stream.cuda_stream), "fastid_merge_topk")
     return s, x
 
 

@@ -186,19 +186,14 @@ extern "C" int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, i
     return FASTID_OK;
 }
 
-extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
-                                   int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
-                                   uint32_t* top_scores, int64_t* top_index, void* workspace,
-                                   size_t workspace_bytes, int formulation, void* stream) {
+extern "C" int fastid_topk_partials(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                    int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
+                                    void* workspace, size_t workspace_bytes, int formulation, void* stream,
+                                    int* n_lists, int* list_len, size_t* index_offset, size_t* score_offset) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
-    if (n_queries == 0) return FASTID_OK;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (n_refs == 0) {
-        FASTID_CUDA(cudaMemsetAsync(top_scores, 0xFF, (size_t)n_queries * k * sizeof(uint32_t), st));
-        FASTID_CUDA(cudaMemsetAsync(top_index, 0xFF, (size_t)n_queries * k * sizeof(int64_t), st));
-        return FASTID_OK;
-    }
+    if (!n_lists || !list_len || !index_offset || !score_offset) FASTID_FAIL(FASTID_E_INVALID, "NULL out-param");
+    if (n_refs == 0 || n_queries == 0) FASTID_FAIL(FASTID_E_INVALID, "empty panels have no partial lists");
     size_t need = 0;
     if (int rc = fastid_topk_workspace(n_refs, n_queries, k, formulation, &need)) return rc;
     if (workspace_bytes < need)
@@ -215,9 +210,35 @@ extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void*
     a.part_index = (int64_t*)(((uintptr_t)workspace + 15) & ~(uintptr_t)15);
     a.part_scores = (uint32_t*)(a.part_index + (size_t)parts * n_queries * kp);
     int launched_parts = 0;
-    if (int rc = launch(kTopK, a, f, &launched_parts, st)) return rc;
+    if (int rc = launch(kTopK, a, f, &launched_parts, (cudaStream_t)stream)) return rc;
     if (launched_parts != parts) FASTID_FAIL(FASTID_E_INVALID, "internal: partition mismatch");
-    return launch_merge(a.part_scores, a.part_index, parts, n_queries, kp, k, top_scores, top_index, st);
+    *n_lists = parts;
+    *list_len = kp;
+    *index_offset = (size_t)((uintptr_t)a.part_index - (uintptr_t)workspace);
+    *score_offset = (size_t)((uintptr_t)a.part_scores - (uintptr_t)workspace);
+    return FASTID_OK;
+}
+
+extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                   int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
+                                   uint32_t* top_scores, int64_t* top_index, void* workspace,
+                                   size_t workspace_bytes, int formulation, void* stream) {
+    if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
+    if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
+    if (n_queries == 0) return FASTID_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_refs == 0) {
+        FASTID_CUDA(cudaMemsetAsync(top_scores, 0xFF, (size_t)n_queries * k * sizeof(uint32_t), st));
+        FASTID_CUDA(cudaMemsetAsync(top_index, 0xFF, (size_t)n_queries * k * sizeof(int64_t), st));
+        return FASTID_OK;
+    }
+    int lists = 0, kp = 0;
+    size_t xo = 0, so = 0;
+    if (int rc = fastid_topk_partials(refs, n_refs, queries, n_queries, stride, bit_length, k, max_score, ref_base,
+                                      workspace, workspace_bytes, formulation, stream, &lists, &kp, &xo, &so))
+        return rc;
+    return launch_merge((const uint32_t*)((uint8_t*)workspace + so), (const int64_t*)((uint8_t*)workspace + xo),
+                        lists, n_queries, kp, k, top_scores, top_index, st);
 }
 
 extern "C" int fastid_compare_threshold(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,

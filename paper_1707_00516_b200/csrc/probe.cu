@@ -1,0 +1,130 @@
+// Pipe-peak probes: the measured roofline denominators for the two
+// formulations.  Each runs one CTA per SM doing
+// nothing but the formulation's inner instruction at its tile shape:
+//   * tensor: back-to-back tcgen05.mma (M=128, N=BN, same kind as the
+//     comparison kernel) on resident shared-memory operands, alternating two
+//     TMEM accumulators, no epilogue;
+//   * popc:   LOP3 (and-not) + POPC + IADD on register-resident words with 16
+//     independent accumulators per thread.
+// Work per launch is returned so the caller divides by CUDA-event time.
+#include "common.cuh"
+#include "tensor_ptx.cuh"
+
+namespace fastid {
+namespace {
+
+template <bool F4>
+__global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* sink) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t done;
+    constexpr int BN = F4 ? 224 : 128;
+    const int warp = threadIdx.x >> 5;
+    // zero operands: A 128 x 32 B, B BN x 32 B (one MMA's K)
+    for (int i = threadIdx.x; i < (128 + BN) * 32 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    ptx::fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&done, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc(&tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (F4) {
+        const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+        ptx::tmem_fill32(lb + 448, 0x7F7F7F7Fu);
+        ptx::tmem_fill32(lb + 480, 0x7F7F7F7Fu);
+        ptx::tmem_wait_st();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (threadIdx.x == 0) {
+        const uint32_t a = ptx::smem_u32(smem);
+        const uint32_t b = a + 128 * 32;
+        const uint64_t ad = ptx::smem_desc(a, 128 * 16, 128);
+        const uint64_t bd = ptx::smem_desc(b, BN * 16, 128);
+        for (int i = 0; i < iters; ++i) {
+            const uint32_t d = tmem + (uint32_t)((i & 1) * BN);
+            if (F4)
+                ptx::mma_mxf4(d, ad, bd, ptx::idesc_mxf4(128, BN), tmem + 448, tmem + 480, i > 1);
+            else
+                ptx::mma_i8(d, ad, bd, ptx::idesc_i8(128, BN), i > 1);
+        }
+        ptx::tc_commit(&done);
+        ptx::mbar_wait(&done, 0);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        uint32_t v[32];
+        // read one accumulator column so the work is observable
+        ptx::tmem_ld32(tmem, v);
+        ptx::tmem_wait_ld();
+        if (threadIdx.x == 0) sink[blockIdx.x] = v[0];
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+__global__ void __launch_bounds__(256) popc_probe_kernel(int iters, uint32_t seed, uint32_t* sink) {
+    uint32_t r[8], acc[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = seed * (threadIdx.x + 17 * i + 1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0;
+    uint32_t q0 = seed ^ threadIdx.x, q1 = seed + blockIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            acc[2 * i] += __popc(r[i] & ~q0);
+            acc[2 * i + 1] += __popc(r[i] & ~q1);
+        }
+        q0 = q0 * 1664525u + 1013904223u;  // keep the words changing (2 IMAD per 16 POPC)
+        q1 = q1 ^ (q0 >> 3);
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i];
+    if (s == 0xDEADBEEF) sink[0] = s;
+}
+
+}  // namespace
+}  // namespace fastid
+
+using namespace fastid;
+
+// Launch the probe for `formulation` with `iters` inner iterations per CTA (tensor)
+// or per thread (popc).  *work receives the bit-pairs (MACs) the launch performs.
+extern "C" int fastid_probe_peak(int formulation, int iters, void* scratch, double* work, void* stream) {
+    int dev = 0, sms = 148;
+    FASTID_CUDA(cudaGetDevice(&dev));
+    FASTID_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t* sink = (uint32_t*)scratch;
+    if (formulation == FASTID_POPC) {
+        const int blocks = sms * 8;
+        popc_probe_kernel<<<blocks, 256, 0, st>>>(iters, 0x9E3779B9u, sink);
+        FASTID_LAUNCHED("popc_probe_kernel");
+        *work = (double)blocks * 256 * iters * 16 * 32;
+        return FASTID_OK;
+    }
+    const bool f4 = formulation == FASTID_TENSOR_F4 || formulation == FASTID_AUTO;
+    const int bn = f4 ? 224 : 128;
+    const int smem = (128 + bn) * 32;
+    if (f4) {
+        FASTID_CUDA(cudaFuncSetAttribute(mma_probe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        mma_probe_kernel<true><<<sms, 128, 200 * 1024, st>>>(iters, sink);
+    } else {
+        FASTID_CUDA(cudaFuncSetAttribute(mma_probe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        mma_probe_kernel<false><<<sms, 128, 200 * 1024, st>>>(iters, sink);
+    }
+    (void)smem;
+    FASTID_LAUNCHED("mma_probe_kernel");
+    const double k = f4 ? 64.0 : 32.0;
+    *work = (double)sms * iters * 128.0 * bn * k;
+    return FASTID_OK;
+}

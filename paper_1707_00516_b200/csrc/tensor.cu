@@ -36,9 +36,11 @@ constexpr int kM = 128;             // unknowns per CTA (MMA M, TMEM lanes)
 constexpr int kStageBytesPacked = 32;  // packed bytes per known row per stage (256 loci)
 constexpr int kWordsPerStage = kStageBytesPacked / 4;
 constexpr int kMaxPackedStages = 12;
-constexpr int kThreads = 320;
 constexpr int kConvThreads = 128;
-constexpr int kEpiThreads = 128;
+constexpr int kEpiWarps = 8;       // two per TMEM lane quadrant, splitting the columns
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kConvThreads + kEpiThreads;  // producer, MMA, converters, epilogue
+constexpr int kChunk = 16;         // accumulator columns per tcgen05.ld
 constexpr int kSmemLimit = 227 * 1024;
 
 template <int F>
@@ -73,6 +75,34 @@ __device__ __forceinline__ void unpack_i8(uint32_t w, uint4& lo, uint4& hi) {
     lo = make_uint4(w & 0x01010101u, (w >> 1) & 0x01010101u, (w >> 2) & 0x01010101u, (w >> 3) & 0x01010101u);
     hi = make_uint4((w >> 4) & 0x01010101u, (w >> 5) & 0x01010101u, (w >> 6) & 0x01010101u,
                     (w >> 7) & 0x01010101u);
+}
+
+// Accumulator encodings.  mxf4 accumulates exact integers in fp32, whose bit
+// patterns order like the integers (non-negative floats); i8 accumulates s32.
+template <int F>
+__device__ __forceinline__ uint32_t score_bits(uint32_t s) {
+    return F == FASTID_TENSOR_F4 ? __float_as_uint((float)s) : s;
+}
+template <int F>
+__device__ __forceinline__ uint32_t decode_exact(uint32_t v) {
+    return F == FASTID_TENSOR_F4 ? (uint32_t)__uint_as_float(v) : v;
+}
+// float -> u32 for integers < 2^23 without F2I: add 2^23, read the mantissa.
+template <int F>
+__device__ __forceinline__ uint32_t decode_fast(uint32_t v) {
+    return F == FASTID_TENSOR_F4 ? __float_as_uint(__uint_as_float(v) + 8388608.0f) - 0x4B000000u : v;
+}
+
+// v[c] for a run-time c without local memory: a 4-level select tree.
+__device__ __forceinline__ uint32_t pick16(const uint32_t (&v)[16], int c) {
+    uint32_t a[8], b[4], d[2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (c & 8) ? v[i + 8] : v[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = (c & 4) ? a[i + 4] : a[i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) d[i] = (c & 2) ? b[i + 2] : b[i];
+    return (c & 1) ? d[1] : d[0];
 }
 
 // Core-matrix offset of (row, core column) in a K-major no-swizzle operand of `rows` rows.
@@ -138,17 +168,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < SP; ++i) {
             ptx::mbar_init(&p_full[i], 1);
-            ptx::mbar_init(&p_empty[i], kConvThreads / 32);
+            ptx::mbar_init(&p_empty[i], kConvThreads);
         }
         for (int i = 0; i < SU; ++i) {
-            ptx::mbar_init(&u_full[i], kConvThreads / 32);
+            ptx::mbar_init(&u_full[i], kConvThreads);
             ptx::mbar_init(&u_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&t_full[i], 1);
             ptx::mbar_init(&t_empty[i], kEpiThreads);
         }
-        ptx::mbar_init(a_full, kConvThreads / 32);
+        ptx::mbar_init(a_full, kConvThreads);
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap);
@@ -247,8 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(a_full);
+            ptx::mbar_arrive(a_full);
         }
         uint32_t it = 0;
         for (int64_t t = t_begin; t < t_end; ++t) {
@@ -265,8 +294,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     v[1][0] = *reinterpret_cast<const uint4*>(P + (ct + 128) * kStageBytesPacked);
                     v[1][1] = *reinterpret_cast<const uint4*>(P + (ct + 128) * kStageBytesPacked + 16);
                 }
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&p_empty[sp]);
                 ptx::mbar_wait(&u_empty[su], ((it / SU) & 1) ^ 1);
                 uint8_t* U = sU + su * UB;
 #pragma unroll
@@ -287,52 +314,93 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+                // every lane arrives itself: its loads of P[sp] have been consumed
+                // by the stores above, and its own fence orders those stores
+                // before the tensor core reads U[su]
+                ptx::mbar_arrive(&p_empty[sp]);
                 ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&u_full[su]);
+                ptx::mbar_arrive(&u_full[su]);
             }
         }
     } else {
         // ---------------- epilogue: one unknown per thread ----------------
-        const int quad = warp & 3;  // the TMEM lane quadrant this warp may access
+        // Warp w reads TMEM lanes 32*(w%4).. (its quadrant) and one half of the
+        // accumulator columns; scores stay as raw accumulator bits (fp32 of an
+        // exact integer is order-preserving as u32), so the hot loop is compares
+        // only and the rare candidates take a warp-uniform slow path.
+        const int ew = warp - 6;
+        const int quad = warp & 3;
+        const int half = ew >> 2;
+        constexpr int kHalfCols = BN / 2;  // 112 (mxf4) or 64 (i8): a multiple of kChunk
         const int m = quad * 32 + lane;
         const int64_t q = q0 + m;
         const bool q_ok = q < a.n_queries;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
         TopList<KP> top;
         if (MODE == kTopK) top.clear();
+        const uint64_t cap = (uint64_t)a.max_score + 1;  // admit v <= max_score
+        uint32_t thr_bits = 0;
+        if (MODE == kTopK) thr_bits = score_bits<F>(cap < kEmptyScore ? (uint32_t)cap : kEmptyScore);
+        const uint32_t hit_bits = MODE == kThreshold ? score_bits<F>(a.threshold) : 0u;
         int local = 0;
         for (int64_t t = t_begin; t < t_end; ++t, ++local) {
             const int acc = local & 1;
             ptx::mbar_wait(&t_full[acc], (local >> 1) & 1);
             ptx::tc_fence_after();
-            const int64_t r0 = t * BN;
+            const int64_t r0 = t * BN + half * kHalfCols;
+            const int64_t rows_left = a.n_refs - r0;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t v[32];
-                ptx::tmem_ld32(lane_base + (uint32_t)(acc * BN + c0), v);
+            for (int ch = 0; ch < kHalfCols / kChunk; ++ch) {
+                uint32_t v[kChunk];
+                ptx::tmem_ld16(lane_base + (uint32_t)(acc * BN + half * kHalfCols + ch * kChunk), v);
                 ptx::tmem_wait_ld();
-                if (c0 + 32 >= BN) {
-                    // last chunk of this accumulator is in registers: hand it back early
+                if (ch + 1 == kHalfCols / kChunk) {
+                    // this warp's half of the accumulator is in registers: release it
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(&t_empty[acc]);
                 }
+                const int64_t rc = r0 + ch * kChunk;
+                const uint32_t valid = !q_ok || rows_left <= ch * kChunk ? 0u
+                                       : (rows_left >= (ch + 1) * kChunk ? 0xFFFFu
+                                                                         : (1u << (rows_left - ch * kChunk)) - 1u);
+                if (MODE == kFull) {
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const uint32_t s = F == FASTID_TENSOR_F4 ? (uint32_t)__uint_as_float(v[c]) : v[c];
-                    const int64_t r = r0 + c0 + c;
-                    if (MODE == kFull) {
-                        if (q_ok && r < a.n_refs) a.out[r * a.ld_out + q] = s;
-                    } else if (MODE == kTopK) {
-                        if (q_ok && r < a.n_refs) top.offer(s, (uint32_t)r, a.max_score);
-                    } else {
-                        emit_hits(a, q_ok && r < a.n_refs && s <= a.threshold, (uint32_t)q, r, s);
+                    for (int c = 0; c < kChunk; ++c)
+                        if ((valid >> c) & 1u) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
+                } else if (MODE == kTopK) {
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int c = 0; c < kChunk; ++c) cand |= (v[c] < thr_bits ? 1u : 0u) << c;
+                    cand &= valid;
+                    // rare: one insertion per loop trip, value picked by a select tree
+                    while (cand) {
+                        const int c = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        const uint32_t vc = pick16(v, c);
+                        if (vc < thr_bits) {
+                            top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
+                            const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
+                            thr_bits = score_bits<F>(w < kEmptyScore ? (uint32_t)w : kEmptyScore);
+                        }
+                    }
+                } else {
+                    uint32_t hit = 0;
+#pragma unroll
+                    for (int c = 0; c < kChunk; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
+                    hit &= valid;
+                    if (__any_sync(0xffffffffu, hit != 0)) {
+                        uint32_t all = __reduce_or_sync(0xffffffffu, hit);
+                        while (all) {  // warp-uniform walk over columns with a hit in any lane
+                            const int c = __ffs(all) - 1;
+                            all &= all - 1;
+                            emit_hits(a, (hit >> c) & 1u, (uint32_t)q, rc + c, decode_exact<F>(pick16(v, c)));
+                        }
                     }
                 }
             }
         }
         if (MODE == kTopK && q_ok) {
-            const int64_t off = ((int64_t)slice * a.n_queries + q) * KP;
+            const int64_t off = (((int64_t)slice * 2 + half) * a.n_queries + q) * KP;
             top.store(a.part_scores + off, a.part_index + off, a.ref_base);
         }
     }
@@ -416,7 +484,7 @@ int launch_fmt(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t strea
     const int slices = slices_for<F>(a.n_refs, a.n_queries);
     if (mode == kFull) return launch_one<F, kFull, 1>(a, slices, stream);
     if (mode == kThreshold) return launch_one<F, kThreshold, 1>(a, slices, stream);
-    *n_parts = slices;
+    *n_parts = 2 * slices;  // one partial list per (slice, epilogue column half)
     switch (a.kpad) {
         case 8: return launch_one<F, kTopK, 8>(a, slices, stream);
         case 16: return launch_one<F, kTopK, 16>(a, slices, stream);
@@ -435,8 +503,8 @@ int tensor_supported(int64_t bit_length, int formulation) {
 }
 
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation) {
-    if (formulation == FASTID_TENSOR_I8) return slices_for<FASTID_TENSOR_I8>(n_refs, n_queries);
-    return slices_for<FASTID_TENSOR_F4>(n_refs, n_queries);
+    if (formulation == FASTID_TENSOR_I8) return 2 * slices_for<FASTID_TENSOR_I8>(n_refs, n_queries);
+    return 2 * slices_for<FASTID_TENSOR_F4>(n_refs, n_queries);
 }
 
 int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream) {

@@ -1,0 +1,139 @@
+"""Database-scale search: a known panel resident in HBM, queried in batches.
+
+This is the shape of the paper's headline job (2048 unknowns x 20M knowns,
+PAPER.md:13): the known database is uploaded once (PAPER.md:151-153 batch
+the knowns because a K80 could not hold them; a B200's 180 GB holds 20M x
+1,024 loci = 2.56 GB seventy times over), and each batch of unknowns is
+scored against all of it with a fused top-k or threshold epilogue, so the
+N_R x N_Q count matrix is never materialised.
+
+``KnownDatabase.search`` is the host-buffer public call: unknowns from host
+memory (pinned staging) -> device, compare + epilogue on the device, results
+back to host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .compare import DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device
+from .panel import ThresholdHits, TopKResult
+
+__all__ = ["KnownDatabase", "QueryStager"]
+
+
+class QueryStager:
+    """Pinned host staging + device buffers for repeated query batches of one shape."""
+
+    def __init__(self, n_queries: int, n_words: int, word_width: int, bit_length: int, k: int, device):
+        self.device = device
+        self.word_width = word_width
+        self.bit_length = bit_length
+        nbytes = n_words * word_width // 8
+        self.host_in = torch.empty((n_queries, nbytes), dtype=torch.uint8).pin_memory()
+        self.dev_in = torch.empty((n_queries, nbytes), dtype=torch.uint8, device=device)
+        self.panel = DevicePanel.empty(n_queries, bit_length, word_width, device)
+        self.out_s = torch.empty((n_queries, k), dtype=torch.int32, device=device)
+        self.out_x = torch.empty((n_queries, k), dtype=torch.int64, device=device)
+        self.host_s = torch.empty((n_queries, k), dtype=torch.int32).pin_memory()
+        self.host_x = torch.empty((n_queries, k), dtype=torch.int64).pin_memory()
+        self.workspace = None
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.host_in.numel()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.host_s.numel() * 4 + self.host_x.numel() * 8
+
+
+class KnownDatabase:
+    """A known panel resident on one device (or one shard of it, ``ref_base`` = global offset)."""
+
+    def __init__(self, refs, bit_length: int | None = None, device=None, ref_base: int = 0,
+                 formulation: str | int = "auto"):
+        self.device = _require_cuda(device)
+        if isinstance(refs, DevicePanel):
+            self.panel = refs
+        elif hasattr(refs, "words"):
+            self.panel = DevicePanel.from_panel(refs, self.device)
+        else:
+            if bit_length is None:
+                raise ValueError("bit_length is required for raw word arrays")
+            self.panel = DevicePanel.from_words(refs, bit_length, device=self.device)
+        self.ref_base = int(ref_base)
+        self.formulation = formulation
+        self._stagers: dict = {}
+
+    @property
+    def n_profiles(self) -> int:
+        return self.panel.n_profiles
+
+    @property
+    def bit_length(self) -> int:
+        return self.panel.bit_length
+
+    def _queries_device(self, queries) -> DevicePanel:
+        if isinstance(queries, DevicePanel):
+            return queries
+        return DevicePanel.from_panel(queries, self.device)
+
+    # -- device-resident calls (inputs already in HBM) -------------------------
+    def topk_device(self, queries: DevicePanel, k: int, max_score: int | None = None, workspace=None, out=None):
+        return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out)
+
+    def full_device(self, queries: DevicePanel, out=None) -> torch.Tensor:
+        return compare_device(self.panel, queries, out, self.formulation)
+
+    # -- host-buffer public calls ------------------------------------------------
+    def stager(self, n_queries: int, k: int) -> QueryStager:
+        key = (n_queries, k)
+        st = self._stagers.get(key)
+        if st is None:
+            p = self.panel
+            st = QueryStager(n_queries, p.n_words, p.word_width, p.bit_length, k, self.device)
+            self._stagers[key] = st
+        return st
+
+    def search_words(self, query_words: np.ndarray, k: int = 16, max_score: int | None = None,
+                     stager: QueryStager | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """Top-k of a (N_Q, N_W) host word array -> host (scores u32 [N_Q,k], index i64 [N_Q,k]).
+
+        Per call: pinned H2D of the unknowns, on-device encode into the row
+        layout, fused compare + top-k, D2H of the (score, index) lists.
+        """
+        p = self.panel
+        qw = np.ascontiguousarray(query_words)
+        if qw.dtype.itemsize * 8 != p.word_width or qw.ndim != 2 or qw.shape[1] != p.n_words:
+            from .errors import PanelMismatchError
+
+            raise PanelMismatchError(f"query words {qw.shape}/{qw.dtype} do not match the database "
+                                     f"({p.n_words} x {p.word_width}-bit words)")
+        n_q = qw.shape[0]
+        st = stager or self.stager(n_q, k)
+        st.host_in.numpy()[:] = qw.view(np.uint8).reshape(n_q, -1)
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            st.dev_in.copy_(st.host_in, non_blocking=True)
+            from . import _native
+
+            _native.check(_native.lib().fastid_load_words(
+                st.dev_in.data_ptr(), n_q, st.dev_in.shape[1], st.panel.rows.data_ptr(), st.panel.stride,
+                stream.cuda_stream), "fastid_load_words")
+            s, x = self.topk_device(st.panel, k, max_score, st.workspace, (st.out_s, st.out_x))
+            st.host_s.copy_(s, non_blocking=True)
+            st.host_x.copy_(x, non_blocking=True)
+            stream.synchronize()
+        return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
+
+    def search(self, queries, k: int = 16, max_score: int | None = None) -> TopKResult:
+        """Per unknown, the k closest knowns by (score asc, global index asc)."""
+        _check_panels(self.bit_length, self.panel.word_width, queries.bit_length, queries.word_width)
+        s, x = self.search_words(np.asarray(queries.words), k, max_score)
+        return TopKResult(tuple(queries.ids), s, x, self.panel.ids)
+
+    def threshold(self, queries, threshold: int, capacity: int | None = None) -> ThresholdHits:
+        return threshold_hits(self.panel, queries, threshold, capacity, self.formulation, self.device,
+                              ref_base=self.ref_base)

@@ -1,0 +1,93 @@
+"""Host-side logic: panel validation, errors, layout helpers (CPU only)."""
+
+import numpy as np
+import pytest
+
+import paper_1707_00516_b200 as fb
+from paper_1707_00516_b200.sharded import shard_range
+
+
+def test_panel_validation_matches_reference_rules():
+    with pytest.raises(fb.CorruptProfileError):
+        fb.Panel(("a",), np.array([[1]], dtype=np.uint32), bit_length=8)
+    with pytest.raises(ValueError):
+        fb.Panel(("a",), np.array([[0, 0]], dtype=np.uint32), bit_length=32)
+    with pytest.raises(ValueError):
+        fb.Panel(("a",), np.array([[0]], dtype=np.int32), bit_length=32)
+    with pytest.raises(ValueError):
+        fb.Panel(("a", "b"), np.zeros((1, 1), np.uint64), 64)
+    p = fb.Panel(("a",), np.array([[0xF0000000]], dtype=np.uint32), 8)
+    assert p.n_profiles == 1 and p.n_words == 1 and p.word_width == 32
+    assert not p.words.flags.writeable
+
+
+def test_relayout_round_trip(rng):
+    w = rng.integers(0, 2**63, (7, 3), dtype=np.uint64)
+    p = fb.Panel(tuple("abcdefg"), w, 192)
+    lay = fb.relayout_queries(p)
+    assert lay.words.shape == (3, 7) and lay.n_queries == 7
+    back = fb.restore_queries(lay)
+    assert np.array_equal(back.words, w) and back.ids == p.ids
+    two = fb.Panel(("x", "y"), np.array([[1, 2], [3, 4]], dtype=np.uint32), 64)
+    assert fb.relayout_queries(two).words.ravel().tolist() == [1, 3, 2, 4]
+
+
+def test_tile_config_validation():
+    fb.TileConfig(16)
+    with pytest.raises(ValueError):
+        fb.TileConfig(17)
+    with pytest.raises(ValueError):
+        fb.TileConfig(64, 0)
+
+
+def test_row_stride():
+    assert fb.row_stride(1) == 16 and fb.row_stride(1024) == 128 and fb.row_stride(5000) == 640
+    for L in range(1, 600, 7):
+        s = fb.row_stride(L)
+        assert s % 16 == 0 and s * 8 >= L and (s - 16) * 8 < L
+
+
+def test_score_matrix_type():
+    m = fb.ScoreMatrix(("r",), ("q0", "q1"), np.array([[1, 2]]))
+    assert m.scores.dtype == np.uint32 and m.shape == (1, 2)
+    with pytest.raises(ValueError):
+        fb.ScoreMatrix(("r",), ("q",), np.zeros((2, 2)))
+
+
+def test_shard_ranges_partition():
+    for n in (0, 1, 7, 20_000_000, 20_000_001):
+        for world in (1, 2, 3, 8):
+            ranges = [shard_range(n, r, world) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+            sizes = [b - a for a, b in ranges]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    r = fb.Panel(("a",), np.zeros((1, 1), np.uint64), 64)
+    with pytest.raises(fb.DeviceError):
+        fb.compare_b200(r, r)
+    with pytest.raises(fb.DeviceError):
+        fb.topk(r, r, 1)
+
+
+def test_mismatch_checked_before_device():
+    a = fb.Panel(("a",), np.zeros((1, 2), np.uint32), 64)
+    b = fb.Panel(("b",), np.zeros((1, 2), np.uint32), 40)
+    with pytest.raises(fb.PanelMismatchError):
+        fb.compare_b200(a, b)
+    c = fb.Panel(("c",), np.zeros((1, 1), np.uint64), 64)
+    with pytest.raises(fb.PanelMismatchError):
+        fb.compare_b200(a, c)
+    with pytest.raises(ValueError):
+        fb.compare_blocked_b200(a, fb.relayout_queries(a), fb.TileConfig(16), 0)
+    # empty panels need no device
+    e = fb.Panel((), np.zeros((0, 2), np.uint32), 64)
+    assert fb.compare_b200(e, a).shape == (0, 1)
