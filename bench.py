@@ -45,7 +45,7 @@ WORKLOAD = "C3: 2048 unknowns x 20M knowns x 1024 SNP loci, fused top-16 per unk
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
     p.add_argument("--n-known", type=int, default=20_000_000)
@@ -169,13 +169,14 @@ def run_reference(args):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.window = None  # (t0, t1) wall-clock of the timed region
         self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"fastid_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
@@ -183,10 +184,15 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(1.5)  # let nvidia-smi start sampling before the timed region
         except Exception:
             self.proc = None
         return self
+
+    def mark(self, start: bool):
+        now = time.time()
+        self.window = (now, None) if start else (self.window[0], now)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -200,22 +206,34 @@ class ClockSampler:
     def summary(self):
         if self.proc is None or not self.path.exists():
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
+        from datetime import datetime
+
+        rows, timed = [], []
         for line in self.path.read_text().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) >= 9 and f[1].replace(".", "").isdigit():
-                rows.append(f)
+            if len(f) < 10 or not f[2].replace(".", "").isdigit():
+                continue
+            rows.append(f)
+            try:
+                ts = datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            if self.window and self.window[0] - 0.05 <= ts <= (self.window[1] or ts) + 0.05:
+                timed.append(f)
         try:
             self.path.unlink()
         except OSError:
             pass
-        if not rows:
+        use = timed or rows
+        if not use:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows]
+        sm = [float(r[2]) for r in use]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+        reasons = sorted({names[i] for r in use for i in range(4) if r[6 + i].lower() == "active"})
+        power = [float(r[4]) for r in use if r[4].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(use[0][3]), "reasons": reasons,
+                "samples": len(use), "samples_in_timed_region": len(timed),
+                "power_w_max": max(power) if power else None}
 
 
 def planted_unknowns(shard_words: np.ndarray, n_unknown: int, L: int, rng) -> tuple[np.ndarray, np.ndarray]:
@@ -329,18 +347,19 @@ def run_b200(args):
     def step(record_kernel: bool):
         if record_kernel:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s, x = m.compare.topk_device(db.panel, dq, k, None, start, formulation, ws, out, events=(e0, e1))
+            s, x = db.topk_device(dq, k, None, ws, out, events=(e0, e1))
             kern_ms.append((e0, e1))
         else:
-            s, x = m.compare.topk_device(db.panel, dq, k, None, start, formulation, ws, out)
+            s, x = db.topk_device(dq, k, None, ws, out)
         return sharded.combine(s, x, k)
 
-    for _ in range(args.warmup):
-        step(False)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step(False)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clocks.mark(True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         for _ in range(args.steps):
@@ -349,6 +368,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
+        clocks.mark(False)
     elapsed = ev0.elapsed_time(ev1) / 1e3
     kernel_s = [a.elapsed_time(b) / 1e3 for a, b in kern_ms]
     if world > 1:

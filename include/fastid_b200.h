@@ -133,6 +133,35 @@ FASTID_API int fastid_merge_topk(const uint32_t* cand_scores, const int64_t* can
                       int64_t n_queries, int k_in, int k, uint32_t* top_scores,
                       int64_t* top_index, void* stream);
 
+/* ---- prepared database (resident known panel + tensor image) ------------- */
+
+/* A known panel prepared for repeated queries: for the tensor formulations
+ * the handle owns a device "tensor image" of the panel -- every known tile
+ * already in the tcgen05 operand layout (e2m1 / u8), built once here -- so the
+ * comparison kernels stream it with bulk copies instead of unpacking bits per
+ * query batch.  The packed rows `refs` must stay alive while the handle does.
+ * Image size: fastid_db_image_bytes (about 4x (mxf4) / 8x (i8) the packed rows). */
+typedef struct fastid_db fastid_db;
+
+FASTID_API size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation);
+FASTID_API int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride, int64_t bit_length,
+                                int formulation, void* stream, fastid_db** out);
+FASTID_API int fastid_db_destroy(fastid_db* db);
+FASTID_API int fastid_db_formulation(const fastid_db* db);
+
+/* As fastid_compare_full / fastid_topk_partials / fastid_compare_threshold with
+ * the database's refs, stride, bit_length and formulation. */
+FASTID_API int fastid_db_compare_full(const fastid_db* db, const void* queries, int64_t n_queries,
+                                      uint32_t* out, int64_t ld_out, void* stream);
+FASTID_API int fastid_db_topk_partials(const fastid_db* db, const void* queries, int64_t n_queries, int k,
+                                       uint32_t max_score, int64_t ref_base, void* workspace,
+                                       size_t workspace_bytes, void* stream, int* n_lists, int* list_len,
+                                       size_t* index_offset, size_t* score_offset);
+FASTID_API int fastid_db_compare_threshold(const fastid_db* db, const void* queries, int64_t n_queries,
+                                           uint32_t threshold, int64_t ref_base, uint32_t* hit_query,
+                                           int64_t* hit_ref, uint32_t* hit_score, int64_t capacity,
+                                           unsigned long long* hit_count, void* stream);
+
 /* ---- host-buffer drop-in (synchronous) ----------------------------------- */
 
 /* Executor.run semantics: ref_words (n_refs x n_words), query_words
@@ -151,6 +180,10 @@ FASTID_API int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
  * with CUDA events on `stream`.  `scratch` is >= 4 * SM-count bytes of device
  * memory. */
 FASTID_API int fastid_probe_peak(int formulation, int iters, void* scratch, double* work, void* stream);
+/* Diagnostic variants of the tensor probe (variant bit 0: one accumulator for
+ * every MMA; bit 1: concurrent 28 KB bulk copies from `src` into shared memory). */
+FASTID_API int fastid_probe_variant(int formulation, int variant, int iters, void* scratch, const void* src,
+                                    int64_t src_bytes, double* work, void* stream);
 
 #ifdef __cplusplus
 }

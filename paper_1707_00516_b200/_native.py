@@ -100,7 +100,16 @@ def lib() -> ctypes.CDLL:
             "fastid_compare_threshold": ([vp, i64, vp, i64, i64, i64, u32, i64, vp, vp, vp, i64, vp, i32, vp], i32),
             "fastid_merge_topk": ([vp, vp, i32, i64, i32, i32, vp, vp, vp], i32),
             "fastid_run_kernel": ([vp, i64, vp, i64, i64, i32, i32, vp, i32], i32),
+            "fastid_db_image_bytes": ([i64, i64, i32], sz),
+            "fastid_db_create": ([vp, i64, i64, i64, i32, vp, ctypes.POINTER(vp)], i32),
+            "fastid_db_destroy": ([vp], i32),
+            "fastid_db_formulation": ([vp], i32),
+            "fastid_db_compare_full": ([vp, vp, i64, vp, i64, vp], i32),
+            "fastid_db_topk_partials": ([vp, vp, i64, i32, u32, i64, vp, sz, vp, ctypes.POINTER(i32),
+                                         ctypes.POINTER(i32), ctypes.POINTER(sz), ctypes.POINTER(sz)], i32),
+            "fastid_db_compare_threshold": ([vp, vp, i64, u32, i64, vp, vp, vp, i64, vp, vp], i32),
             "fastid_probe_peak": ([i32, i32, vp, ctypes.POINTER(ctypes.c_double), vp], i32),
+            "fastid_probe_variant": ([i32, i32, i32, vp, vp, i64, ctypes.POINTER(ctypes.c_double), vp], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

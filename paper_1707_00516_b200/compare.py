@@ -231,7 +231,7 @@ def _ptr(p: DevicePanel) -> int:
 
 
 def compare_device(refs: DevicePanel, queries: DevicePanel, out: torch.Tensor | None = None,
-                   formulation: str | int = "auto") -> torch.Tensor:
+                   formulation: str | int = "auto", image=None) -> torch.Tensor:
     """Full (N_R, N_Q) u32 score matrix on the device (int32 storage, reinterpret as u32)."""
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
     dev = refs.device
@@ -243,10 +243,15 @@ def compare_device(refs: DevicePanel, queries: DevicePanel, out: torch.Tensor | 
         raise ValueError("out rows must be contiguous")
     if refs.n_profiles and queries.n_profiles:
         with torch.cuda.device(dev):
-            _native.check(_native.lib().fastid_compare_full(
-                _ptr(refs), refs.n_profiles, _ptr(queries), queries.n_profiles, refs.stride,
-                refs.bit_length, out.data_ptr(), out.stride(0), _native.formulation_code(formulation),
-                _stream(dev)), "fastid_compare_full")
+            if image is not None:
+                _native.check(_native.lib().fastid_db_compare_full(
+                    image.handle, _ptr(queries), queries.n_profiles, out.data_ptr(), out.stride(0), _stream(dev)),
+                    "fastid_db_compare_full")
+            else:
+                _native.check(_native.lib().fastid_compare_full(
+                    _ptr(refs), refs.n_profiles, _ptr(queries), queries.n_profiles, refs.stride,
+                    refs.bit_length, out.data_ptr(), out.stride(0), _native.formulation_code(formulation),
+                    _stream(dev)), "fastid_compare_full")
     return out
 
 
@@ -330,7 +335,7 @@ def topk_workspace_bytes(n_refs: int, n_queries: int, k: int, formulation: str |
 
 def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int | None = None,
                 ref_base: int = 0, formulation: str | int = "auto", workspace: torch.Tensor | None = None,
-                out: tuple | None = None, events: tuple | None = None):
+                out: tuple | None = None, events: tuple | None = None, image=None):
     """Fused compare + top-k on the device -> (scores int32 [N_Q, k] as u32, index int64 [N_Q, k]).
 
     Two launches on the current stream: the comparison kernel (writing
@@ -364,10 +369,16 @@ def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int 
         stream = torch.cuda.current_stream(dev)
         if events is not None:
             events[0].record(stream)
-        _native.check(L.fastid_topk_partials(
-            _ptr(refs), refs.n_profiles, _ptr(queries), n_q, refs.stride, refs.bit_length, k, ms, ref_base,
-            workspace.data_ptr(), workspace.numel(), _native.formulation_code(formulation), stream.cuda_stream,
-            ctypes.byref(lists), ctypes.byref(kp), ctypes.byref(xo), ctypes.byref(so)), "fastid_topk_partials")
+        if image is not None:
+            _native.check(L.fastid_db_topk_partials(
+                image.handle, _ptr(queries), n_q, k, ms, ref_base, workspace.data_ptr(), workspace.numel(),
+                stream.cuda_stream, ctypes.byref(lists), ctypes.byref(kp), ctypes.byref(xo), ctypes.byref(so)),
+                "fastid_db_topk_partials")
+        else:
+            _native.check(L.fastid_topk_partials(
+                _ptr(refs), refs.n_profiles, _ptr(queries), n_q, refs.stride, refs.bit_length, k, ms, ref_base,
+                workspace.data_ptr(), workspace.numel(), _native.formulation_code(formulation), stream.cuda_stream,
+                ctypes.byref(lists), ctypes.byref(kp), ctypes.byref(xo), ctypes.byref(so)), "fastid_topk_partials")
         if events is not None:
             events[1].record(stream)
         base = workspace.data_ptr()
@@ -389,7 +400,7 @@ def topk(refs, queries, k: int, max_score: int | None = None, formulation: str |
 
 
 def threshold_hits(refs, queries, threshold: int, capacity: int | None = None,
-                   formulation: str | int = "auto", device=None, ref_base: int = 0) -> ThresholdHits:
+                   formulation: str | int = "auto", device=None, ref_base: int = 0, image=None) -> ThresholdHits:
     """Every (unknown j, known i, score) with score <= threshold, ordered by (j, i)."""
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
     dev = _require_cuda(device)
@@ -401,10 +412,15 @@ def threshold_hits(refs, queries, threshold: int, capacity: int | None = None,
         hr = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
         hs = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
         with torch.cuda.device(dev):
-            _native.check(_native.lib().fastid_compare_threshold(
-                _ptr(dr), dr.n_profiles, _ptr(dq), dq.n_profiles, dr.stride, dr.bit_length, int(threshold),
-                ref_base, hq.data_ptr(), hr.data_ptr(), hs.data_ptr(), cap, count.data_ptr(),
-                _native.formulation_code(formulation), _stream(dev)), "fastid_compare_threshold")
+            if image is not None:
+                _native.check(_native.lib().fastid_db_compare_threshold(
+                    image.handle, _ptr(dq), dq.n_profiles, int(threshold), ref_base, hq.data_ptr(), hr.data_ptr(),
+                    hs.data_ptr(), cap, count.data_ptr(), _stream(dev)), "fastid_db_compare_threshold")
+            else:
+                _native.check(_native.lib().fastid_compare_threshold(
+                    _ptr(dr), dr.n_profiles, _ptr(dq), dq.n_profiles, dr.stride, dr.bit_length, int(threshold),
+                    ref_base, hq.data_ptr(), hr.data_ptr(), hs.data_ptr(), cap, count.data_ptr(),
+                    _native.formulation_code(formulation), _stream(dev)), "fastid_compare_threshold")
         n = int(count.item())
         if n <= cap:
             break

@@ -157,17 +157,27 @@ extern "C" int fastid_supports(int formulation, int64_t bit_length) {
     return tensor_supported(bit_length, formulation) ? 1 : 0;
 }
 
-extern "C" int fastid_compare_full(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
-                                   int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out,
-                                   int formulation, void* stream) {
+namespace {
+int compare_full_impl(const void* refs, const void* image, int64_t n_refs, const void* queries, int64_t n_queries,
+                      int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out, int formulation,
+                      void* stream) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (ld_out < n_queries) FASTID_FAIL(FASTID_E_INVALID, "ld_out smaller than n_queries");
     if (n_refs == 0 || n_queries == 0) return FASTID_OK;
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
+    a.image = (const uint8_t*)image;
     a.out = out;
     a.ld_out = ld_out;
     int parts = 0;
     return launch(kFull, a, resolve_formulation(formulation, bit_length), &parts, (cudaStream_t)stream);
+}
+}  // namespace
+
+extern "C" int fastid_compare_full(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                   int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out,
+                                   int formulation, void* stream) {
+    return compare_full_impl(refs, nullptr, n_refs, queries, n_queries, stride, bit_length, out, ld_out, formulation,
+                             stream);
 }
 
 extern "C" int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, int formulation, size_t* bytes) {
@@ -186,10 +196,11 @@ extern "C" int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, i
     return FASTID_OK;
 }
 
-extern "C" int fastid_topk_partials(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
-                                    int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
-                                    void* workspace, size_t workspace_bytes, int formulation, void* stream,
-                                    int* n_lists, int* list_len, size_t* index_offset, size_t* score_offset) {
+namespace {
+int topk_partials_impl(const void* refs, const void* image, int64_t n_refs, const void* queries, int64_t n_queries,
+                       int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
+                       void* workspace, size_t workspace_bytes, int formulation, void* stream, int* n_lists,
+                       int* list_len, size_t* index_offset, size_t* score_offset) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
     if (!n_lists || !list_len || !index_offset || !score_offset) FASTID_FAIL(FASTID_E_INVALID, "NULL out-param");
@@ -203,6 +214,7 @@ extern "C" int fastid_topk_partials(const void* refs, int64_t n_refs, const void
     const int kp = list_size_for(k);
     const int parts = parts_for(f, n_refs, n_queries);
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
+    a.image = (const uint8_t*)image;
     a.k = k;
     a.kpad = kp;
     a.max_score = max_score;
@@ -217,6 +229,16 @@ extern "C" int fastid_topk_partials(const void* refs, int64_t n_refs, const void
     *index_offset = (size_t)((uintptr_t)a.part_index - (uintptr_t)workspace);
     *score_offset = (size_t)((uintptr_t)a.part_scores - (uintptr_t)workspace);
     return FASTID_OK;
+}
+}  // namespace
+
+extern "C" int fastid_topk_partials(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                    int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
+                                    void* workspace, size_t workspace_bytes, int formulation, void* stream,
+                                    int* n_lists, int* list_len, size_t* index_offset, size_t* score_offset) {
+    return topk_partials_impl(refs, nullptr, n_refs, queries, n_queries, stride, bit_length, k, max_score, ref_base,
+                              workspace, workspace_bytes, formulation, stream, n_lists, list_len, index_offset,
+                              score_offset);
 }
 
 extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
@@ -241,17 +263,18 @@ extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void*
                         lists, n_queries, kp, k, top_scores, top_index, st);
 }
 
-extern "C" int fastid_compare_threshold(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
-                                        int64_t stride, int64_t bit_length, uint32_t threshold, int64_t ref_base,
-                                        uint32_t* hit_query, int64_t* hit_ref, uint32_t* hit_score,
-                                        int64_t capacity, unsigned long long* hit_count, int formulation,
-                                        void* stream) {
+namespace {
+int threshold_impl(const void* refs, const void* image, int64_t n_refs, const void* queries, int64_t n_queries,
+                   int64_t stride, int64_t bit_length, uint32_t threshold, int64_t ref_base, uint32_t* hit_query,
+                   int64_t* hit_ref, uint32_t* hit_score, int64_t capacity, unsigned long long* hit_count,
+                   int formulation, void* stream) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (capacity < 0 || !hit_count) FASTID_FAIL(FASTID_E_INVALID, "bad hit buffers");
     cudaStream_t st = (cudaStream_t)stream;
     FASTID_CUDA(cudaMemsetAsync(hit_count, 0, sizeof(unsigned long long), st));
     if (n_refs == 0 || n_queries == 0) return FASTID_OK;
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
+    a.image = (const uint8_t*)image;
     a.threshold = threshold;
     a.ref_base = ref_base;
     a.hit_query = hit_query;
@@ -261,6 +284,101 @@ extern "C" int fastid_compare_threshold(const void* refs, int64_t n_refs, const 
     a.hit_count = hit_count;
     int parts = 0;
     return launch(kThreshold, a, resolve_formulation(formulation, bit_length), &parts, st);
+}
+}  // namespace
+
+extern "C" int fastid_compare_threshold(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
+                                        int64_t stride, int64_t bit_length, uint32_t threshold, int64_t ref_base,
+                                        uint32_t* hit_query, int64_t* hit_ref, uint32_t* hit_score,
+                                        int64_t capacity, unsigned long long* hit_count, int formulation,
+                                        void* stream) {
+    return threshold_impl(refs, nullptr, n_refs, queries, n_queries, stride, bit_length, threshold, ref_base,
+                          hit_query, hit_ref, hit_score, capacity, hit_count, formulation, stream);
+}
+
+// ---- prepared database --------------------------------------------------------
+
+struct fastid_db {
+    const void* refs;
+    int64_t n_refs, stride, bit_length;
+    int formulation;  // resolved
+    void* image;      // owned; null for the CUDA-core formulation
+    size_t image_bytes;
+    int device;
+};
+
+extern "C" size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation) {
+    if (n_refs <= 0 || bit_length <= 0) return 0;
+    const int f = resolve_formulation(formulation, bit_length);
+    return f == FASTID_POPC ? 0 : tensor_image_bytes(n_refs, bit_length, f);
+}
+
+extern "C" int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride, int64_t bit_length,
+                                int formulation, void* stream, fastid_db** out) {
+    if (!out) FASTID_FAIL(FASTID_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (int rc = check_compare(refs, n_refs, refs, 0, stride, bit_length, formulation)) return rc;
+    auto* db = new fastid_db{refs, n_refs, stride, bit_length, resolve_formulation(formulation, bit_length),
+                             nullptr, 0, 0};
+    cudaGetDevice(&db->device);
+    if (db->formulation != FASTID_POPC && n_refs > 0) {
+        db->image_bytes = tensor_image_bytes(n_refs, bit_length, db->formulation);
+        if (cudaMalloc(&db->image, db->image_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            const size_t want = db->image_bytes;
+            delete db;
+            FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the %zu-byte tensor image", want);
+        }
+        CompareArgs a = make_args(refs, n_refs, refs, 0, stride, bit_length);
+        if (int rc = build_tensor_image(a, db->formulation, db->image, (cudaStream_t)stream)) {
+            cudaFree(db->image);
+            delete db;
+            return rc;
+        }
+    }
+    *out = db;
+    return FASTID_OK;
+}
+
+extern "C" int fastid_db_destroy(fastid_db* db) {
+    if (!db) return FASTID_OK;
+    if (db->image) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(db->device);
+        cudaFree(db->image);
+        cudaSetDevice(cur);
+    }
+    delete db;
+    return FASTID_OK;
+}
+
+extern "C" int fastid_db_formulation(const fastid_db* db) { return db ? db->formulation : -1; }
+
+extern "C" int fastid_db_compare_full(const fastid_db* db, const void* queries, int64_t n_queries, uint32_t* out,
+                                      int64_t ld_out, void* stream) {
+    if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    return compare_full_impl(db->refs, db->image, db->n_refs, queries, n_queries, db->stride, db->bit_length, out,
+                             ld_out, db->formulation, stream);
+}
+
+extern "C" int fastid_db_topk_partials(const fastid_db* db, const void* queries, int64_t n_queries, int k,
+                                       uint32_t max_score, int64_t ref_base, void* workspace, size_t workspace_bytes,
+                                       void* stream, int* n_lists, int* list_len, size_t* index_offset,
+                                       size_t* score_offset) {
+    if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    return topk_partials_impl(db->refs, db->image, db->n_refs, queries, n_queries, db->stride, db->bit_length, k,
+                              max_score, ref_base, workspace, workspace_bytes, db->formulation, stream, n_lists,
+                              list_len, index_offset, score_offset);
+}
+
+extern "C" int fastid_db_compare_threshold(const fastid_db* db, const void* queries, int64_t n_queries,
+                                           uint32_t threshold, int64_t ref_base, uint32_t* hit_query,
+                                           int64_t* hit_ref, uint32_t* hit_score, int64_t capacity,
+                                           unsigned long long* hit_count, void* stream) {
+    if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    return threshold_impl(db->refs, db->image, db->n_refs, queries, n_queries, db->stride, db->bit_length, threshold,
+                          ref_base, hit_query, hit_ref, hit_score, capacity, hit_count, db->formulation, stream);
 }
 
 extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries,

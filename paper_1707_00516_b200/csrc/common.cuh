@@ -104,6 +104,8 @@ struct CompareArgs {
     int64_t n_queries;
     int64_t stride;      // bytes per row, multiple of 16
     int64_t bit_length;
+    // optional pre-unpacked tensor image of the refs (prepared database), else null
+    const uint8_t* image;
     // full matrix
     uint32_t* out;
     int64_t ld_out;
@@ -152,6 +154,8 @@ int popc_parts(int64_t n_refs, int64_t n_queries);
 int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream);
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation);
 int tensor_supported(int64_t bit_length, int formulation);
+size_t tensor_image_bytes(int64_t n_refs, int64_t bit_length, int formulation);
+int build_tensor_image(const CompareArgs& a, int formulation, void* image, cudaStream_t stream);
 int launch_merge(const uint32_t* cand_scores, const int64_t* cand_index, int n_lists,
                  int64_t n_queries, int k_in, int k, uint32_t* top_scores, int64_t* top_index,
                  cudaStream_t stream);

@@ -13,11 +13,17 @@
 namespace fastid {
 namespace {
 
+// variant bit 0: accumulate every MMA into ONE accumulator (K-loop dependency)
+// variant bit 1: warp 1 streams bulk copies (28 KB) from `src` into a 4-deep
+//                shared-memory ring while the MMAs run (operand-fill traffic)
 template <bool F4>
-__global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* sink) {
+__global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* sink, int variant,
+                                                           const uint8_t* src, int64_t src_bytes) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t done;
+    __shared__ __align__(8) uint64_t ring_full[4];
+    __shared__ __align__(8) uint64_t ring_empty[4];
     constexpr int BN = F4 ? 224 : 128;
     const int warp = threadIdx.x >> 5;
     // zero operands: A 128 x 32 B, B BN x 32 B (one MMA's K)
@@ -26,6 +32,10 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* 
     ptx::fence_proxy_async_smem();
     if (threadIdx.x == 0) {
         ptx::mbar_init(&done, 1);
+        for (int i = 0; i < 4; ++i) {
+            ptx::mbar_init(&ring_full[i], 1);
+            ptx::mbar_init(&ring_empty[i], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 0) ptx::tmem_alloc(&tmem_slot, 512);
@@ -48,7 +58,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* 
         const uint64_t ad = ptx::smem_desc(a, 128 * 16, 128);
         const uint64_t bd = ptx::smem_desc(b, BN * 16, 128);
         for (int i = 0; i < iters; ++i) {
-            const uint32_t d = tmem + (uint32_t)((i & 1) * BN);
+            const uint32_t d = tmem + (uint32_t)(((variant & 1) ? 0 : (i & 1)) * BN);
             if (F4)
                 ptx::mma_mxf4(d, ad, bd, ptx::idesc_mxf4(128, BN), tmem + 448, tmem + 480, i > 1);
             else
@@ -56,6 +66,26 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* 
         }
         ptx::tc_commit(&done);
         ptx::mbar_wait(&done, 0);
+    } else if ((variant & 2) && threadIdx.x == 32) {
+        // stream 28 KB blocks into the ring until the MMAs finish (stop flag = done phase)
+        constexpr uint32_t kBlk = 28 * 1024;
+        uint8_t* ring = smem + 16 * 1024;
+        int64_t off = (int64_t)blockIdx.x * kBlk;
+        int i = 0;
+        for (;; ++i) {
+            const int s = i & 3;
+            const uint32_t ph = (i >> 2) & 1;
+            if (i >= 4) ptx::mbar_wait(&ring_full[s], ph ^ 1);  // previous fill of this slot landed
+            uint32_t ready = 0;
+            asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(ready) : "r"(ptx::smem_u32(&done)), "r"(0u) : "memory");
+            if (ready) break;
+            ptx::mbar_expect_tx(&ring_full[s], kBlk);
+            ptx::bulk_load(ring + s * kBlk, src + off, kBlk, &ring_full[s]);
+            off += 148 * kBlk;
+            if (off + kBlk > src_bytes) off = (int64_t)blockIdx.x * kBlk;
+        }
+        for (int j = i > 4 ? i - 4 : 0; j < i; ++j) ptx::mbar_wait(&ring_full[j & 3], (j >> 2) & 1);  // drain
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -99,7 +129,15 @@ using namespace fastid;
 
 // Launch the probe for `formulation` with `iters` inner iterations per CTA (tensor)
 // or per thread (popc).  *work receives the bit-pairs (MACs) the launch performs.
+extern "C" int fastid_probe_variant(int formulation, int variant, int iters, void* scratch, const void* src,
+                                    int64_t src_bytes, double* work, void* stream);
+
 extern "C" int fastid_probe_peak(int formulation, int iters, void* scratch, double* work, void* stream) {
+    return fastid_probe_variant(formulation, 0, iters, scratch, nullptr, 0, work, stream);
+}
+
+extern "C" int fastid_probe_variant(int formulation, int variant, int iters, void* scratch, const void* src,
+                                    int64_t src_bytes, double* work, void* stream) {
     int dev = 0, sms = 148;
     FASTID_CUDA(cudaGetDevice(&dev));
     FASTID_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -117,10 +155,10 @@ extern "C" int fastid_probe_peak(int formulation, int iters, void* scratch, doub
     const int smem = (128 + bn) * 32;
     if (f4) {
         FASTID_CUDA(cudaFuncSetAttribute(mma_probe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        mma_probe_kernel<true><<<sms, 128, 200 * 1024, st>>>(iters, sink);
+        mma_probe_kernel<true><<<sms, 128, 200 * 1024, st>>>(iters, sink, variant, (const uint8_t*)src, src_bytes);
     } else {
         FASTID_CUDA(cudaFuncSetAttribute(mma_probe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        mma_probe_kernel<false><<<sms, 128, 200 * 1024, st>>>(iters, sink);
+        mma_probe_kernel<false><<<sms, 128, 200 * 1024, st>>>(iters, sink, variant, (const uint8_t*)src, src_bytes);
     }
     (void)smem;
     FASTID_LAUNCHED("mma_probe_kernel");

@@ -26,6 +26,8 @@
 // from L2.  DESIGN.md has the roofline and byte accounting.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tensor_ptx.cuh"
 
@@ -36,7 +38,12 @@ constexpr int kM = 128;             // unknowns per CTA (MMA M, TMEM lanes)
 constexpr int kStageBytesPacked = 32;  // packed bytes per known row per stage (256 loci)
 constexpr int kWordsPerStage = kStageBytesPacked / 4;
 constexpr int kMaxPackedStages = 12;
-constexpr int kConvThreads = 128;
+constexpr int kMinPackedStages = 4;
+constexpr int kMaxUnpackedStages = 6;
+constexpr int kMaxAStages = 4;
+constexpr int kConvWarps = 8;      // two per SMSP: halves the per-stage unpack latency
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kFirstEpiWarp = 2 + kConvWarps;
 constexpr int kEpiWarps = 8;       // two per TMEM lane quadrant, splitting the columns
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kConvThreads + kEpiThreads;  // producer, MMA, converters, epilogue
@@ -50,7 +57,6 @@ struct Fmt<FASTID_TENSOR_I8> {
     static constexpr int BN = 128;          // knowns per tile (MMA N)
     static constexpr int kCoresPerWord = 2; // 16-B core columns produced per packed u32
     static constexpr int kMmaPerStage = 8;  // K = 32 B of operand per MMA
-    static constexpr int kUnpackedStages = 2;
     static constexpr int kTmemCols = 256;   // 2 x BN accumulator columns
 };
 template <>
@@ -58,7 +64,6 @@ struct Fmt<FASTID_TENSOR_F4> {
     static constexpr int BN = 224;
     static constexpr int kCoresPerWord = 1;
     static constexpr int kMmaPerStage = 4;
-    static constexpr int kUnpackedStages = 2;
     static constexpr int kTmemCols = 512;   // 2 x 224 accumulators + 64 scale-factor columns
 };
 
@@ -66,31 +71,63 @@ constexpr uint32_t kSfaCol = 448;  // mxf4: unit scale factors for A (32 columns
 constexpr uint32_t kSfbCol = 480;  // mxf4: unit scale factors for B (32 columns)
 constexpr uint32_t kUnitScales = 0x7F7F7F7Fu;  // ue8m0 127 = 2^0
 
-// e2m1 nibbles (1.0 = 0x2): nibble n of word j <- bit 4n + j.
+// Operand encodings.  K element (n, j) of a packed word w is bit 4n + j
+// (mxf4: nibble n of output word j) or bit 8b + j (i8: byte b of output
+// word j); A and B use the same order, so the dot product runs over the
+// same loci.  To keep the per-tile (B = known) unpack to masks, B keeps each
+// bit where it lies, and the resident A operand (unknowns, built once per
+// CTA) carries the reciprocal weight, so every product a_k * b_k is exactly
+// a uniform constant:
+//   mxf4: B nibble values 0.5 / 1 / 2 / 2 (bits 0,1,2 and bit 3 moved to 2)
+//         A nibble values 2 / 1 / 0.5 / 0.5            -> product 1.0
+//   i8:   B byte values 2^j, A byte values 2^(7-j)      -> product 128
+template <bool B_SIDE>
 __device__ __forceinline__ uint4 unpack_f4(uint32_t w) {
-    return make_uint4((w << 1) & 0x22222222u, w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
+    if (B_SIDE) {
+        // w >> 1 on the FMA pipe: high word of w * 2^31
+        return make_uint4(w & 0x11111111u, w & 0x22222222u, w & 0x44444444u,
+                          __umulhi(w, 0x80000000u) & 0x44444444u);
+    }
+    return make_uint4((w << 2) & 0x44444444u, w & 0x22222222u, (w >> 2) & 0x11111111u, (w >> 3) & 0x11111111u);
 }
-// int8 bytes (1 = 0x01): byte b of word j <- bit 8b + j; two 16-B core columns.
+template <bool B_SIDE>
 __device__ __forceinline__ void unpack_i8(uint32_t w, uint4& lo, uint4& hi) {
-    lo = make_uint4(w & 0x01010101u, (w >> 1) & 0x01010101u, (w >> 2) & 0x01010101u, (w >> 3) & 0x01010101u);
-    hi = make_uint4((w >> 4) & 0x01010101u, (w >> 5) & 0x01010101u, (w >> 6) & 0x01010101u,
-                    (w >> 7) & 0x01010101u);
+    if (B_SIDE) {
+        lo = make_uint4(w & 0x01010101u, w & 0x02020202u, w & 0x04040404u, w & 0x08080808u);
+        hi = make_uint4(w & 0x10101010u, w & 0x20202020u, w & 0x40404040u, w & 0x80808080u);
+        return;
+    }
+    // byte b of word j = bit (8b + j) << (7 - j)
+    lo = make_uint4((w << 7) & 0x80808080u, (w << 5) & 0x40404040u, (w << 3) & 0x20202020u, (w << 1) & 0x10101010u);
+    hi = make_uint4((w >> 1) & 0x08080808u, (w >> 3) & 0x04040404u, (w >> 5) & 0x02020202u, (w >> 7) & 0x01010101u);
 }
 
 // Accumulator encodings.  mxf4 accumulates exact integers in fp32, whose bit
 // patterns order like the integers (non-negative floats); i8 accumulates s32.
 template <int F>
 __device__ __forceinline__ uint32_t score_bits(uint32_t s) {
-    return F == FASTID_TENSOR_F4 ? __float_as_uint((float)s) : s;
+    // i8 accumulates 128 * score; saturate thresholds above the representable range
+    return F == FASTID_TENSOR_F4 ? __float_as_uint((float)s) : (s >= (1u << 24) ? 0xFFFFFFFFu : s << 7);
 }
 template <int F>
 __device__ __forceinline__ uint32_t decode_exact(uint32_t v) {
-    return F == FASTID_TENSOR_F4 ? (uint32_t)__uint_as_float(v) : v;
+    return F == FASTID_TENSOR_F4 ? (uint32_t)__uint_as_float(v) : v >> 7;
 }
 // float -> u32 for integers < 2^23 without F2I: add 2^23, read the mantissa.
 template <int F>
 __device__ __forceinline__ uint32_t decode_fast(uint32_t v) {
-    return F == FASTID_TENSOR_F4 ? __float_as_uint(__uint_as_float(v) + 8388608.0f) - 0x4B000000u : v;
+    return F == FASTID_TENSOR_F4 ? __float_as_uint(__uint_as_float(v) + 8388608.0f) - 0x4B000000u : v >> 7;
+}
+
+// Unsigned minimum of 16 values with 3-input mins (raw fp32 bits of
+// non-negative floats order like the floats).
+__device__ __forceinline__ uint32_t min16(const uint32_t (&v)[16]) {
+    uint32_t a = __vimin3_u32(v[0], v[1], v[2]);
+    uint32_t b = __vimin3_u32(v[3], v[4], v[5]);
+    uint32_t c = __vimin3_u32(v[6], v[7], v[8]);
+    uint32_t d = __vimin3_u32(v[9], v[10], v[11]);
+    uint32_t e = __vimin3_u32(v[12], v[13], v[14]);
+    return __vimin3_u32(__vimin3_u32(a, b, c), __vimin3_u32(d, e, v[15]), 0xFFFFFFFFu);
 }
 
 // v[c] for a run-time c without local memory: a 4-level select tree.
@@ -105,6 +142,20 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&v)[16], int c) {
     return (c & 1) ? d[1] : d[0];
 }
 
+// Position in a ring of mbarrier-guarded stages: slot index + phase parity.
+struct Ring {
+    int idx;
+    uint32_t phase;
+    int n;
+    __device__ explicit Ring(int n_) : idx(0), phase(0), n(n_) {}
+    __device__ __forceinline__ void next() {
+        if (++idx == n) {
+            idx = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
 // Core-matrix offset of (row, core column) in a K-major no-swizzle operand of `rows` rows.
 __device__ __forceinline__ uint32_t core_off(int row, int col, int rows) {
     return (uint32_t)col * (uint32_t)(rows * 16) + (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u;
@@ -115,34 +166,65 @@ struct Layout {
     static constexpr int BN = Fmt<F>::BN;
     static constexpr int kUnpackedStageBytes = BN * 16 * kWordsPerStage * Fmt<F>::kCoresPerWord;
     static constexpr int kPackedStageBytes = BN * kStageBytesPacked;
+    static constexpr int kAStageBytes = kM * 16 * kWordsPerStage * Fmt<F>::kCoresPerWord;
+    static constexpr int kBarBytes = 8 * (2 * kMaxPackedStages + 2 * kMaxUnpackedStages + 2 * kMaxAStages + 5) + 16;
     int n_kst;    // stages per tile (K padded to 256 loci)
-    int a_bytes;  // resident complemented unknown tile
-    int sp;       // packed ring depth that fits
+    int a_bytes;  // resident A tile, or the A ring when streaming
+    int sa;       // A ring depth (streamed A only)
+    int su;       // operand ring depth (converter or TMA -> MMA)
+    int sp;       // packed ring depth (TMA -> converter); 0 with a tensor image
+    bool img;
     int off_u, off_p, off_bar, total;
-    __host__ __device__ explicit Layout(int64_t stride) {
+    __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false) {
         n_kst = (int)((stride + kStageBytesPacked - 1) / kStageBytesPacked);
-        a_bytes = n_kst * kWordsPerStage * Fmt<F>::kCoresPerWord * kM * 16;
-        off_u = a_bytes;
-        off_p = off_u + Fmt<F>::kUnpackedStages * kUnpackedStageBytes;
-        const int bar_bytes = 8 * (2 * kMaxPackedStages + 2 * Fmt<F>::kUnpackedStages + 5) + 16;
-        int room = (kSmemLimit - off_p - bar_bytes) / kPackedStageBytes;
-        sp = room > kMaxPackedStages ? kMaxPackedStages : room;
-        off_bar = off_p + (sp > 0 ? sp : 0) * kPackedStageBytes;
-        total = off_bar + bar_bytes;
+        img = image;
+        sa = 0;
+        if (!stream_a) {
+            a_bytes = n_kst * kAStageBytes;
+            place();
+        } else {
+            for (sa = kMaxAStages; sa >= 2; --sa) {
+                a_bytes = sa * kAStageBytes;
+                place();
+                if (fits()) break;
+            }
+        }
     }
+    __host__ __device__ void place() {
+        const int room = kSmemLimit - a_bytes - kBarBytes;
+        if (img) {
+            // the tensor image is already in the UMMA layout: only the operand ring
+            su = room / kUnpackedStageBytes;
+            if (su > kMaxUnpackedStages) su = kMaxUnpackedStages;
+            sp = 0;
+        } else {
+            // deepest unpacked ring that still leaves kMinPackedStages TMA stages
+            su = (room - kMinPackedStages * kPackedStageBytes) / kUnpackedStageBytes;
+            if (su > kMaxUnpackedStages) su = kMaxUnpackedStages;
+            sp = su >= 2 ? (room - su * kUnpackedStageBytes) / kPackedStageBytes : 0;
+            if (sp > kMaxPackedStages) sp = kMaxPackedStages;
+        }
+        off_u = a_bytes;
+        off_p = off_u + (su > 0 ? su : 0) * kUnpackedStageBytes;
+        off_bar = off_p + (sp > 0 ? sp : 0) * kPackedStageBytes;
+        total = off_bar + kBarBytes;
+    }
+    __host__ __device__ bool fits() const { return su >= 2 && (img || sp >= 2) && total <= kSmemLimit; }
 };
 
-template <int F, int MODE, int KP>
+template <int F, int MODE, int KP, bool SA, bool IMG>
 __global__ void __launch_bounds__(kThreads, 1)
-    tensor_kernel(const __grid_constant__ CUtensorMap tmap, CompareArgs a, int64_t n_tiles, int n_slices) {
+    tensor_kernel(const __grid_constant__ CUtensorMap tmap, CompareArgs a, const uint8_t* __restrict__ a_global,
+                  int64_t n_tiles, int n_slices) {
     constexpr int BN = Fmt<F>::BN;
-    constexpr int SU = Fmt<F>::kUnpackedStages;
     constexpr int CPW = Fmt<F>::kCoresPerWord;
     constexpr int UB = Layout<F>::kUnpackedStageBytes;
     constexpr int PB = Layout<F>::kPackedStageBytes;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const Layout<F> lay(a.stride);
+    const Layout<F> lay(a.stride, SA, IMG);
+    constexpr int AB = Layout<F>::kAStageBytes;
     const int SP = lay.sp;
+    const int SU = lay.su;
     const int n_kst = lay.n_kst;
     uint8_t* sA = smem;
     uint8_t* sU = smem + lay.off_u;
@@ -151,11 +233,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* p_full = bars;
     uint64_t* p_empty = p_full + kMaxPackedStages;
     uint64_t* u_full = p_empty + kMaxPackedStages;
-    uint64_t* u_empty = u_full + SU;
-    uint64_t* t_full = u_empty + SU;
+    uint64_t* u_empty = u_full + kMaxUnpackedStages;
+    uint64_t* t_full = u_empty + kMaxUnpackedStages;
     uint64_t* t_empty = t_full + 2;
     uint64_t* a_full = t_empty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 1);
+    uint64_t* ar_full = a_full + 1;  // streamed-A ring
+    uint64_t* ar_empty = ar_full + kMaxAStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ar_empty + kMaxAStages);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -171,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&p_empty[i], kConvThreads);
         }
         for (int i = 0; i < SU; ++i) {
-            ptx::mbar_init(&u_full[i], kConvThreads);
+            ptx::mbar_init(&u_full[i], IMG ? 1 : kConvThreads);
             ptx::mbar_init(&u_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -179,6 +263,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&t_empty[i], kEpiThreads);
         }
         ptx::mbar_init(a_full, kConvThreads);
+        for (int i = 0; i < kMaxAStages; ++i) {
+            ptx::mbar_init(&ar_full[i], 1);
+            ptx::mbar_init(&ar_empty[i], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap);
@@ -187,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (F == FASTID_TENSOR_F4 && warp >= 6) {
+    if (F == FASTID_TENSOR_F4 && warp >= kFirstEpiWarp) {
         // unit block scales (ue8m0 127) for every MMA: whole SF region, all lanes
         const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         ptx::tmem_fill32(lb + kSfaCol, kUnitScales);
@@ -201,11 +289,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            uint32_t it = 0;
+            Ring ra(SA ? lay.sa : 1), rp(SP > 0 ? SP : 1), ru(SU);
             for (int64_t t = t_begin; t < t_end; ++t) {
-                for (int ks = 0; ks < n_kst; ++ks, ++it) {
-                    const int s = (int)(it % (uint32_t)SP);
-                    ptx::mbar_wait(&p_empty[s], ((it / SP) & 1) ^ 1);
+                for (int ks = 0; ks < n_kst; ++ks, rp.next()) {
+                    if (SA) {
+                        // this stage's slice of the pre-unpacked A operand (one bulk copy)
+                        const int sa = ra.idx;
+                        ptx::mbar_wait(&ar_empty[sa], ra.phase ^ 1);
+                        ptx::mbar_expect_tx(&ar_full[sa], AB);
+                        ptx::bulk_load(sA + sa * AB, a_global + ((int64_t)group * n_kst + ks) * AB, AB, &ar_full[sa]);
+                        ra.next();
+                    }
+                    if (IMG) {
+                        // the known tile's stage, already unpacked: one bulk copy into the operand ring
+                        ptx::mbar_wait(&u_empty[ru.idx], ru.phase ^ 1);
+                        ptx::mbar_expect_tx(&u_full[ru.idx], UB);
+                        ptx::bulk_load(sU + ru.idx * UB, a.image + (t * n_kst + ks) * (int64_t)UB, UB,
+                                       &u_full[ru.idx]);
+                        ru.next();
+                        continue;
+                    }
+                    const int s = rp.idx;
+                    ptx::mbar_wait(&p_empty[s], rp.phase ^ 1);
                     ptx::mbar_expect_tx(&p_full[s], PB);
                     ptx::tma_load_2d(sP + s * PB, &tmap, &p_full[s], ks * kStageBytesPacked, (int)(t * BN));
                 }
@@ -217,23 +322,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc = F == FASTID_TENSOR_F4 ? ptx::idesc_mxf4(kM, BN) : ptx::idesc_i8(kM, BN);
             const uint32_t a_base = ptx::smem_u32(sA);
             const uint32_t u_base = ptx::smem_u32(sU);
-            ptx::mbar_wait(a_full, 0);
+            if (!SA) ptx::mbar_wait(a_full, 0);
             ptx::tc_fence_after();
-            uint32_t it = 0;
+            Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
             for (int64_t t = t_begin; t < t_end; ++t, ++local) {
                 const int acc = local & 1;
                 ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
-                for (int ks = 0; ks < n_kst; ++ks, ++it) {
-                    const int s = (int)(it % SU);
-                    ptx::mbar_wait(&u_full[s], (it / SU) & 1);
+                for (int ks = 0; ks < n_kst; ++ks, ru.next()) {
+                    const int s = ru.idx;
+                    const int sa = ra.idx;
+                    if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
+                    ptx::mbar_wait(&u_full[s], ru.phase);
                     ptx::tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < Fmt<F>::kMmaPerStage; ++kk) {
-                        const uint32_t acol = (uint32_t)(ks * kWordsPerStage * CPW + 2 * kk);
-                        const uint64_t ad = ptx::smem_desc(a_base + acol * (kM * 16), kM * 16, 128);
+                        const uint32_t acol = SA ? (uint32_t)(2 * kk) : (uint32_t)(ks * kWordsPerStage * CPW + 2 * kk);
+                        const uint32_t abase = SA ? a_base + (uint32_t)(sa * AB) : a_base;
+                        const uint64_t ad = ptx::smem_desc(abase + acol * (kM * 16), kM * 16, 128);
                         const uint64_t bd =
                             ptx::smem_desc(u_base + s * UB + (uint32_t)(2 * kk) * (BN * 16), BN * 16, 128);
                         const uint32_t accum = (ks | kk) ? 1u : 0u;
@@ -243,74 +351,85 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::mma_i8(d, ad, bd, idesc, accum);
                     }
                     ptx::tc_commit(&u_empty[s]);  // stage s reusable once these MMAs retire
+                    if (SA) {
+                        ptx::tc_commit(&ar_empty[sa]);
+                        ra.next();
+                    }
                 }
                 ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < kFirstEpiWarp) {
         // ---------------- converters ----------------
-        const int ct = threadIdx.x - 64;  // 0..127
+        const int ct = threadIdx.x - 64;  // 0..kConvThreads-1
         {
-            // Resident A = complemented unknown row ct; zero past the row.
-            const int64_t q = q0 + ct;
-            const bool real = q < a.n_queries;
-            const int row_words = (int)(a.stride / 4);
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(a.queries + (real ? q : 0) * a.stride);
-            for (int w4 = 0; w4 < n_kst * kWordsPerStage; w4 += 4) {
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (real && w4 < row_words) {
-                    v = *reinterpret_cast<const uint4*>(src + w4);
-                    v = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
-                }
-                const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+            // Resident A = complemented unknown rows; zero past the row.  Threads
+            // 0..127 each build one row.
+            if (!SA && ct < kM) {
+                const int64_t q = q0 + ct;
+                const bool real = q < a.n_queries;
+                const int row_words = (int)(a.stride / 4);
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(a.queries + (real ? q : 0) * a.stride);
+                for (int w4 = 0; w4 < n_kst * kWordsPerStage; w4 += 4) {
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (real && w4 < row_words) {
+                        v = *reinterpret_cast<const uint4*>(src + w4);
+                        v = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
+                    }
+                    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int col = (w4 + i) * CPW;
-                    if (F == FASTID_TENSOR_F4) {
-                        *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) = unpack_f4(wv[i]);
-                    } else {
-                        uint4 lo, hi;
-                        unpack_i8(wv[i], lo, hi);
-                        *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) = lo;
-                        *reinterpret_cast<uint4*>(sA + core_off(ct, col + 1, kM)) = hi;
+                    for (int i = 0; i < 4; ++i) {
+                        const int col = (w4 + i) * CPW;
+                        if (F == FASTID_TENSOR_F4) {
+                            *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) = unpack_f4<false>(wv[i]);
+                        } else {
+                            uint4 lo, hi;
+                            unpack_i8<false>(wv[i], lo, hi);
+                            *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) = lo;
+                            *reinterpret_cast<uint4*>(sA + core_off(ct, col + 1, kM)) = hi;
+                        }
                     }
                 }
             }
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(a_full);
         }
-        uint32_t it = 0;
+        if (IMG) goto converters_done;
+        {
+        // Work unit = (known row, 16-byte half of the stage): 2*BN units per stage.
+        constexpr int kUnits = 2 * BN;
+        constexpr int kUnitsPerThread = (kUnits + kConvThreads - 1) / kConvThreads;
+        Ring rp(SP), ru(SU);
         for (int64_t t = t_begin; t < t_end; ++t) {
-            for (int ks = 0; ks < n_kst; ++ks, ++it) {
-                const int sp = (int)(it % (uint32_t)SP);
-                const int su = (int)(it % SU);
-                ptx::mbar_wait(&p_full[sp], (it / SP) & 1);
+            for (int ks = 0; ks < n_kst; ++ks, rp.next(), ru.next()) {
+                const int sp = rp.idx;
+                const int su = ru.idx;
+                ptx::mbar_wait(&p_full[sp], rp.phase);
                 const uint8_t* P = sP + sp * PB;
-                const bool second = ct + 128 < BN;
-                uint4 v[2][2];
-                v[0][0] = *reinterpret_cast<const uint4*>(P + ct * kStageBytesPacked);
-                v[0][1] = *reinterpret_cast<const uint4*>(P + ct * kStageBytesPacked + 16);
-                if (second) {
-                    v[1][0] = *reinterpret_cast<const uint4*>(P + (ct + 128) * kStageBytesPacked);
-                    v[1][1] = *reinterpret_cast<const uint4*>(P + (ct + 128) * kStageBytesPacked + 16);
+                uint4 v[kUnitsPerThread];
+#pragma unroll
+                for (int h = 0; h < kUnitsPerThread; ++h) {
+                    const int u = ct + kConvThreads * h;
+                    if (u < kUnits) v[h] = *reinterpret_cast<const uint4*>(P + u * 16);
                 }
-                ptx::mbar_wait(&u_empty[su], ((it / SU) & 1) ^ 1);
+                ptx::mbar_wait(&u_empty[su], ru.phase ^ 1);
                 uint8_t* U = sU + su * UB;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && !second) break;
-                    const int row = ct + 128 * h;
-                    const uint32_t wv[8] = {v[h][0].x, v[h][0].y, v[h][0].z, v[h][0].w,
-                                            v[h][1].x, v[h][1].y, v[h][1].z, v[h][1].w};
+                for (int h = 0; h < kUnitsPerThread; ++h) {
+                    const int u = ct + kConvThreads * h;
+                    if (u >= kUnits) break;
+                    const int row = u >> 1;
+                    const int col0 = (u & 1) * 4 * CPW;
+                    const uint32_t wv[4] = {v[h].x, v[h].y, v[h].z, v[h].w};
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
+                    for (int i = 0; i < 4; ++i) {
                         if (F == FASTID_TENSOR_F4) {
-                            *reinterpret_cast<uint4*>(U + core_off(row, i, BN)) = unpack_f4(wv[i]);
+                            *reinterpret_cast<uint4*>(U + core_off(row, col0 + i, BN)) = unpack_f4<true>(wv[i]);
                         } else {
                             uint4 lo, hi;
-                            unpack_i8(wv[i], lo, hi);
-                            *reinterpret_cast<uint4*>(U + core_off(row, 2 * i, BN)) = lo;
-                            *reinterpret_cast<uint4*>(U + core_off(row, 2 * i + 1, BN)) = hi;
+                            unpack_i8<true>(wv[i], lo, hi);
+                            *reinterpret_cast<uint4*>(U + core_off(row, col0 + 2 * i, BN)) = lo;
+                            *reinterpret_cast<uint4*>(U + core_off(row, col0 + 2 * i + 1, BN)) = hi;
                         }
                     }
                 }
@@ -322,13 +441,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_arrive(&u_full[su]);
             }
         }
+        }
+    converters_done:;
     } else {
         // ---------------- epilogue: one unknown per thread ----------------
         // Warp w reads TMEM lanes 32*(w%4).. (its quadrant) and one half of the
         // accumulator columns; scores stay as raw accumulator bits (fp32 of an
         // exact integer is order-preserving as u32), so the hot loop is compares
         // only and the rare candidates take a warp-uniform slow path.
-        const int ew = warp - 6;
+        const int ew = warp - kFirstEpiWarp;
         const int quad = warp & 3;
         const int half = ew >> 2;
         constexpr int kHalfCols = BN / 2;  // 112 (mxf4) or 64 (i8): a multiple of kChunk
@@ -349,6 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const int64_t r0 = t * BN + half * kHalfCols;
             const int64_t rows_left = a.n_refs - r0;
+            // rows of this half that exist (0 for padding unknowns); full tiles skip masking
+            const int rl = !q_ok ? 0 : (rows_left >= kHalfCols ? kHalfCols : (rows_left > 0 ? (int)rows_left : 0));
+            const bool full = rl == kHalfCols;
 #pragma unroll 1
             for (int ch = 0; ch < kHalfCols / kChunk; ++ch) {
                 uint32_t v[kChunk];
@@ -360,34 +484,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_arrive(&t_empty[acc]);
                 }
                 const int64_t rc = r0 + ch * kChunk;
-                const uint32_t valid = !q_ok || rows_left <= ch * kChunk ? 0u
-                                       : (rows_left >= (ch + 1) * kChunk ? 0xFFFFu
-                                                                         : (1u << (rows_left - ch * kChunk)) - 1u);
+                const int left = rl - ch * kChunk;
+                const uint32_t valid =
+                    full || left >= kChunk ? 0xFFFFu : (left <= 0 ? 0u : (1u << left) - 1u);
                 if (MODE == kFull) {
 #pragma unroll
                     for (int c = 0; c < kChunk; ++c)
-                        if ((valid >> c) & 1u) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
+                        if (full || ((valid >> c) & 1u)) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
                 } else if (MODE == kTopK) {
-                    uint32_t cand = 0;
+                    // common case: one min over the chunk, one compare (3-input mins)
+                    if (!full && valid != 0xFFFFu) {
 #pragma unroll
-                    for (int c = 0; c < kChunk; ++c) cand |= (v[c] < thr_bits ? 1u : 0u) << c;
-                    cand &= valid;
-                    // rare: one insertion per loop trip, value picked by a select tree
-                    while (cand) {
-                        const int c = __ffs(cand) - 1;
-                        cand &= cand - 1;
-                        const uint32_t vc = pick16(v, c);
-                        if (vc < thr_bits) {
-                            top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
-                            const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
-                            thr_bits = score_bits<F>(w < kEmptyScore ? (uint32_t)w : kEmptyScore);
+                        for (int c = 0; c < kChunk; ++c)
+                            if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
+                    }
+                    if (min16(v) < thr_bits) {
+                        uint32_t cand = 0;
+#pragma unroll
+                        for (int c = 0; c < kChunk; ++c) cand |= (v[c] < thr_bits ? 1u : 0u) << c;
+                        // rare: one insertion per loop trip, value picked by a select tree
+                        while (cand) {
+                            const int c = __ffs(cand) - 1;
+                            cand &= cand - 1;
+                            const uint32_t vc = pick16(v, c);
+                            if (vc < thr_bits) {
+                                top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
+                                const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
+                                thr_bits = score_bits<F>(w < kEmptyScore ? (uint32_t)w : kEmptyScore);
+                            }
                         }
                     }
                 } else {
-                    uint32_t hit = 0;
+                    if (!full && valid != 0xFFFFu) {
 #pragma unroll
-                    for (int c = 0; c < kChunk; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
-                    hit &= valid;
+                        for (int c = 0; c < kChunk; ++c)
+                            if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
+                    }
+                    const bool any = min16(v) <= hit_bits;
+                    uint32_t hit = 0;
+                    if (any) {
+#pragma unroll
+                        for (int c = 0; c < kChunk; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
+                    }
                     if (__any_sync(0xffffffffu, hit != 0)) {
                         uint32_t all = __reduce_or_sync(0xffffffffu, hit);
                         while (all) {  // warp-uniform walk over columns with a hit in any lane
@@ -463,19 +601,130 @@ int slices_for(int64_t n_refs, int64_t n_queries) {
     return (int)s;
 }
 
-template <int F, int MODE, int KP>
-int launch_one(const CompareArgs& a, int n_slices, cudaStream_t stream) {
+// Streamed-A operand: complemented, unpacked unknown rows laid out stage by
+// stage ([group][stage][core matrices]) so each stage is one bulk copy.
+template <int F>
+__global__ void prep_a_kernel(CompareArgs a, int n_groups, int n_kst, uint8_t* __restrict__ out) {
+    constexpr int CPW = Fmt<F>::kCoresPerWord;
+    constexpr int AB = Layout<F>::kAStageBytes;
+    const int64_t total = (int64_t)n_groups * n_kst * kM;
+    const int row_words = (int)(a.stride / 4);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int row = (int)(t % kM);
+        const int64_t gs = t / kM;  // group * n_kst + stage
+        const int ks = (int)(gs % n_kst);
+        const int64_t q = (gs / n_kst) * kM + row;
+        const bool real = q < a.n_queries;
+        uint8_t* dst = out + gs * AB;
+#pragma unroll
+        for (int w = 0; w < kWordsPerStage; ++w) {
+            const int word = ks * kWordsPerStage + w;
+            uint32_t x = 0;
+            if (real && word < row_words) x = ~reinterpret_cast<const uint32_t*>(a.queries + q * a.stride)[word];
+            if (F == FASTID_TENSOR_F4) {
+                *reinterpret_cast<uint4*>(dst + core_off(row, w, kM)) = unpack_f4<false>(x);
+            } else {
+                uint4 lo, hi;
+                unpack_i8<false>(x, lo, hi);
+                *reinterpret_cast<uint4*>(dst + core_off(row, 2 * w, kM)) = lo;
+                *reinterpret_cast<uint4*>(dst + core_off(row, 2 * w + 1, kM)) = hi;
+            }
+        }
+    }
+}
+
+template <int F>
+bool use_stream_a(int64_t stride) { return !Layout<F>(stride, false).fits(); }
+
+template <int F, int MODE, int KP, bool SA, bool IMG>
+int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     CUtensorMap map;
     if (int rc = make_known_map(&map, a, Fmt<F>::BN)) return rc;
-    const Layout<F> lay(a.stride);
-    if (lay.sp < 2 || lay.total > kSmemLimit)
-        FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
-    auto kern = tensor_kernel<F, MODE, KP>;
+    const Layout<F> lay(a.stride, SA, IMG);
+    if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
+    auto kern = tensor_kernel<F, MODE, KP, SA, IMG>;
     FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     const int64_t groups = ceil_div(a.n_queries, kM);
     const int64_t tiles = ceil_div(a.n_refs, Fmt<F>::BN);
-    kern<<<(unsigned)(groups * n_slices), kThreads, lay.total, stream>>>(map, a, tiles, n_slices);
+    uint8_t* a_global = nullptr;
+    if (SA) {
+        const size_t bytes = (size_t)groups * lay.n_kst * Layout<F>::kAStageBytes;
+        FASTID_CUDA(cudaMallocAsync((void**)&a_global, bytes, stream));
+        const int64_t work = groups * lay.n_kst * kM;
+        prep_a_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 16), 256, 0, stream>>>(
+            a, (int)groups, lay.n_kst, a_global);
+        FASTID_LAUNCHED("prep_a_kernel");
+    }
+    kern<<<(unsigned)(groups * n_slices), kThreads, lay.total, stream>>>(map, a, a_global, tiles, n_slices);
     FASTID_LAUNCHED("tensor_kernel");
+    if (SA) FASTID_CUDA(cudaFreeAsync(a_global, stream));
+    return FASTID_OK;
+}
+
+template <int F, int MODE, int KP>
+int launch_one(const CompareArgs& a, int n_slices, cudaStream_t stream) {
+    const bool img = a.image != nullptr;
+    const bool sa = !Layout<F>(a.stride, false, img).fits();
+    if (img) {
+        if (sa) return launch_one_impl<F, MODE, KP, true, true>(a, n_slices, stream);
+        return launch_one_impl<F, MODE, KP, false, true>(a, n_slices, stream);
+    }
+    if (sa) return launch_one_impl<F, MODE, KP, true, false>(a, n_slices, stream);
+    return launch_one_impl<F, MODE, KP, false, false>(a, n_slices, stream);
+}
+
+// Tensor image of a known panel: for every (tile, stage) the UMMA-layout B
+// operand block the converters would produce, written once at database load.
+template <int F>
+__global__ void build_image_kernel(CompareArgs a, int64_t n_tiles, int n_kst, uint8_t* __restrict__ image) {
+    constexpr int BN = Fmt<F>::BN;
+    constexpr int CPW = Fmt<F>::kCoresPerWord;
+    constexpr int UB = Layout<F>::kUnpackedStageBytes;
+    const int64_t total = n_tiles * n_kst * 2 * BN;  // units: (tile, stage, row, 16-B half)
+    const int64_t row_bytes = a.stride;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
+        const int unit = (int)(u % (2 * BN));
+        const int64_t blk = u / (2 * BN);  // tile * n_kst + stage
+        const int ks = (int)(blk % n_kst);
+        const int64_t tile = blk / n_kst;
+        const int row = unit >> 1;
+        const int half = unit & 1;
+        const int64_t r = tile * BN + row;
+        const int64_t off = (int64_t)ks * kStageBytesPacked + half * 16;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < a.n_refs && off < row_bytes) v = *reinterpret_cast<const uint4*>(a.refs + r * row_bytes + off);
+        uint8_t* dst = image + blk * UB;
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        const int col0 = half * 4 * CPW;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (F == FASTID_TENSOR_F4) {
+                *reinterpret_cast<uint4*>(dst + core_off(row, col0 + i, BN)) = unpack_f4<true>(wv[i]);
+            } else {
+                uint4 lo, hi;
+                unpack_i8<true>(wv[i], lo, hi);
+                *reinterpret_cast<uint4*>(dst + core_off(row, col0 + 2 * i, BN)) = lo;
+                *reinterpret_cast<uint4*>(dst + core_off(row, col0 + 2 * i + 1, BN)) = hi;
+            }
+        }
+    }
+}
+
+template <int F>
+size_t image_bytes_fmt(int64_t n_refs, int64_t stride) {
+    const Layout<F> lay(stride, false, true);
+    return (size_t)ceil_div(n_refs, Fmt<F>::BN) * lay.n_kst * Layout<F>::kUnpackedStageBytes;
+}
+
+template <int F>
+int build_image_fmt(const CompareArgs& a, void* image, cudaStream_t stream) {
+    const Layout<F> lay(a.stride, false, true);
+    const int64_t tiles = ceil_div(a.n_refs, Fmt<F>::BN);
+    const int64_t work = tiles * lay.n_kst * 2 * Fmt<F>::BN;
+    if (work == 0) return FASTID_OK;
+    build_image_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 32), 256, 0, stream>>>(
+        a, tiles, lay.n_kst, (uint8_t*)image);
+    FASTID_LAUNCHED("build_image_kernel");
     return FASTID_OK;
 }
 
@@ -497,9 +746,24 @@ int launch_fmt(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t strea
 
 int tensor_supported(int64_t bit_length, int formulation) {
     const int64_t stride = row_stride_bytes(bit_length);
-    if (formulation == FASTID_TENSOR_I8) return Layout<FASTID_TENSOR_I8>(stride).sp >= 2;
-    if (formulation == FASTID_TENSOR_F4) return Layout<FASTID_TENSOR_F4>(stride).sp >= 2;
+    if (formulation == FASTID_TENSOR_I8)
+        return Layout<FASTID_TENSOR_I8>(stride, false).fits() || Layout<FASTID_TENSOR_I8>(stride, true).fits();
+    if (formulation == FASTID_TENSOR_F4)
+        return Layout<FASTID_TENSOR_F4>(stride, false).fits() || Layout<FASTID_TENSOR_F4>(stride, true).fits();
     return 0;
+}
+
+size_t tensor_image_bytes(int64_t n_refs, int64_t bit_length, int formulation) {
+    const int64_t stride = row_stride_bytes(bit_length);
+    if (formulation == FASTID_TENSOR_I8) return image_bytes_fmt<FASTID_TENSOR_I8>(n_refs, stride);
+    if (formulation == FASTID_TENSOR_F4) return image_bytes_fmt<FASTID_TENSOR_F4>(n_refs, stride);
+    return 0;
+}
+
+int build_tensor_image(const CompareArgs& a, int formulation, void* image, cudaStream_t stream) {
+    if (formulation == FASTID_TENSOR_I8) return build_image_fmt<FASTID_TENSOR_I8>(a, image, stream);
+    if (formulation == FASTID_TENSOR_F4) return build_image_fmt<FASTID_TENSOR_F4>(a, image, stream);
+    FASTID_FAIL(FASTID_E_INVALID, "no tensor image for formulation %d", formulation);
 }
 
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation) {

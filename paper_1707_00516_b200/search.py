@@ -14,13 +14,49 @@ back to host.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
 from .compare import DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device
 from .panel import ThresholdHits, TopKResult
 
-__all__ = ["KnownDatabase", "QueryStager"]
+__all__ = ["KnownDatabase", "PreparedImage", "QueryStager"]
+
+
+class PreparedImage:
+    """Owner of a C-ABI ``fastid_db`` handle: the known panel's tensor image.
+
+    For the tcgen05 formulations the image holds every known tile already in
+    the MMA operand layout (e2m1 nibbles / u8 bytes, ~4x / 8x the packed
+    rows), so query batches stream it with bulk copies and no per-batch bit
+    unpacking.  Built once per database (fastid_db_create).
+    """
+
+    def __init__(self, panel: DevicePanel, formulation: str | int):
+        from . import _native
+
+        self.panel = panel  # keeps the packed rows alive for the handle
+        self.handle = ctypes.c_void_p()
+        L = _native.lib()
+        with torch.cuda.device(panel.device):
+            _native.check(L.fastid_db_create(panel.rows.data_ptr() if panel.n_profiles else 0, panel.n_profiles,
+                                             panel.stride, panel.bit_length, _native.formulation_code(formulation),
+                                             torch.cuda.current_stream(panel.device).cuda_stream,
+                                             ctypes.byref(self.handle)), "fastid_db_create")
+        self.formulation = L.fastid_db_formulation(self.handle)
+        self.image_bytes = L.fastid_db_image_bytes(panel.n_profiles, panel.bit_length, self.formulation)
+
+    def __del__(self):
+        try:
+            from . import _native
+
+            if self.handle:
+                _native.lib().fastid_db_destroy(self.handle)
+                self.handle = ctypes.c_void_p()
+        except Exception:
+            pass
 
 
 class QueryStager:
@@ -53,7 +89,7 @@ class KnownDatabase:
     """A known panel resident on one device (or one shard of it, ``ref_base`` = global offset)."""
 
     def __init__(self, refs, bit_length: int | None = None, device=None, ref_base: int = 0,
-                 formulation: str | int = "auto"):
+                 formulation: str | int = "auto", prepare: bool = True):
         self.device = _require_cuda(device)
         if isinstance(refs, DevicePanel):
             self.panel = refs
@@ -66,6 +102,8 @@ class KnownDatabase:
         self.ref_base = int(ref_base)
         self.formulation = formulation
         self._stagers: dict = {}
+        # the tensor image (built once) lets every query batch skip bit unpacking
+        self.image = PreparedImage(self.panel, formulation) if prepare and self.panel.n_profiles else None
 
     @property
     def n_profiles(self) -> int:
@@ -81,11 +119,13 @@ class KnownDatabase:
         return DevicePanel.from_panel(queries, self.device)
 
     # -- device-resident calls (inputs already in HBM) -------------------------
-    def topk_device(self, queries: DevicePanel, k: int, max_score: int | None = None, workspace=None, out=None):
-        return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out)
+    def topk_device(self, queries: DevicePanel, k: int, max_score: int | None = None, workspace=None, out=None,
+                    events=None):
+        return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out,
+                           events=events, image=self.image)
 
     def full_device(self, queries: DevicePanel, out=None) -> torch.Tensor:
-        return compare_device(self.panel, queries, out, self.formulation)
+        return compare_device(self.panel, queries, out, self.formulation, image=self.image)
 
     # -- host-buffer public calls ------------------------------------------------
     def stager(self, n_queries: int, k: int) -> QueryStager:
@@ -136,4 +176,4 @@ class KnownDatabase:
 
     def threshold(self, queries, threshold: int, capacity: int | None = None) -> ThresholdHits:
         return threshold_hits(self.panel, queries, threshold, capacity, self.formulation, self.device,
-                              ref_base=self.ref_base)
+                              ref_base=self.ref_base, image=self.image)

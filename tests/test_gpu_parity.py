@@ -191,3 +191,56 @@ def test_load_words_roundtrip(rng):
         d = m.DevicePanel.from_words(w, L)
         assert d.stride % 16 == 0 and d.stride == m.row_stride(L)
         assert np.array_equal(d.to_words(), w)
+
+
+@pytest.mark.parametrize("form", FORMS)
+@pytest.mark.parametrize("L", [2048, 2049, 5000, 40000])
+def test_long_profiles_exact(rng, form, L):
+    """Large accumulations stay exact (scores up to L), incl. the streamed-A path."""
+    m = fb()
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, 300, nw, 64, L)
+    q, _ = rand_words(rng, 140, nw, 64, L)
+    # extremes: an all-ones known (score L vs the all-zero unknown), dense/sparse rows
+    r[0] = np.uint64(2**64 - 1)
+    r = oracle.mask_padding(r, L)
+    q[0] = 0
+    r[1] &= r[2]
+    q[1] |= q[2]
+    R, Q = m.Panel(tuple(range(300)), r, L), m.Panel(tuple(range(140)), q, L)
+    exp = oracle.naive(r, q)
+    assert exp[0, 0] == L
+    got = m.compare_b200(R, Q, formulation=form).scores
+    assert np.array_equal(got, exp), (form, L)
+    res = m.topk(R, Q, 8, formulation=form)
+    es, ex, _ = oracle.topk_from_matrix(exp, 8)
+    assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex)
+
+
+@pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8", "popc"])
+@pytest.mark.parametrize("L", [300, 1024, 5000])
+def test_prepared_database_image(rng, form, L):
+    """KnownDatabase (fastid_db handle, tensor image) == oracle for top-k, full matrix and threshold."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, 2500, nw, 64, L)
+    q, _ = rand_words(rng, 150, nw, 64, L)
+    q[:30] = r[rng.integers(0, 2500, 30)]
+    r[1000:1003] = r[:3]
+    db = KnownDatabase(r, L, formulation=form, ref_base=1000)
+    if form != "popc":
+        assert db.image.image_bytes > 0
+    dq = m.DevicePanel.from_words(q, L)
+    full = db.full_device(dq).cpu().numpy().view(np.uint32)
+    exp = oracle.naive(r, q)
+    assert np.array_equal(full, exp)
+    s, x = db.search_words(q, 16)
+    es, ex, _ = oracle.topk_from_matrix(exp, 16)
+    assert np.array_equal(s, es)
+    assert np.array_equal(x, np.where(ex >= 0, ex + 1000, -1))
+    thr = int(np.percentile(exp, 1))
+    hits = db.threshold(m.Panel(tuple(range(150)), q, L), thr)
+    hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
+    assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 1000) and np.array_equal(hits.score, hs)
