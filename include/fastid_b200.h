@@ -182,6 +182,14 @@ FASTID_API int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
 FASTID_API int fastid_probe_peak(int formulation, int iters, void* scratch, double* work, void* stream);
 /* Diagnostic variants of the tensor probe (variant bit 0: one accumulator for
  * every MMA; bit 1: concurrent 28 KB bulk copies from `src` into shared memory). */
+/* Diagnostic: trace CTA 0 of subsequent tensor launches (35 clock64 stamps per
+ * tile for the first `tiles` tiles; see TraceSlot in csrc/common.cuh); NULL = off. */
+FASTID_API int fastid_debug_trace(long long* device_buf, int tiles);
+/* Diagnostic: timing-experiment switches (bit 0: epilogue skips TMEM loads; results invalid). */
+FASTID_API int fastid_debug_flags(int flags);
+FASTID_API int fastid_probe_tmem_read(int x, int warps, int iters, void* scratch, double* work, void* stream);
+/* Diagnostic: MMA stream concurrent with `readers` warps of TMEM loads; sink = 2*SMs u64. */
+FASTID_API int fastid_probe_contention(int iters, int readers, void* sink, void* stream);
 FASTID_API int fastid_probe_variant(int formulation, int variant, int iters, void* scratch, const void* src,
                                     int64_t src_bytes, double* work, void* stream);
 

@@ -109,6 +109,10 @@ def lib() -> ctypes.CDLL:
                                          ctypes.POINTER(i32), ctypes.POINTER(sz), ctypes.POINTER(sz)], i32),
             "fastid_db_compare_threshold": ([vp, vp, i64, u32, i64, vp, vp, vp, i64, vp, vp], i32),
             "fastid_probe_peak": ([i32, i32, vp, ctypes.POINTER(ctypes.c_double), vp], i32),
+            "fastid_probe_tmem_read": ([i32, i32, i32, vp, ctypes.POINTER(ctypes.c_double), vp], i32),
+            "fastid_debug_trace": ([vp, i32], i32),
+            "fastid_debug_flags": ([i32], i32),
+            "fastid_probe_contention": ([i32, i32, vp, vp], i32),
             "fastid_probe_variant": ([i32, i32, i32, vp, vp, i64, ctypes.POINTER(ctypes.c_double), vp], i32),
         }
         for name, (args, res) in sig.items():

@@ -51,9 +51,16 @@ int check_compare(const void* refs, int64_t n_refs, const void* queries, int64_t
     return FASTID_OK;
 }
 
+long long* g_trace = nullptr;
+int g_trace_tiles = 0;
+int g_debug_flags = 0;
+
 CompareArgs make_args(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries, int64_t stride,
                       int64_t bit_length) {
     CompareArgs a{};
+    a.trace = g_trace;
+    a.trace_tiles = g_trace_tiles;
+    a.debug_flags = g_debug_flags;
     a.refs = (const uint8_t*)refs;
     a.queries = (const uint8_t*)queries;
     a.n_refs = n_refs;
@@ -148,6 +155,20 @@ __global__ void transpose_words_kernel(const uint8_t* __restrict__ src, int64_t 
 using namespace fastid;
 
 extern "C" int fastid_abi_version(void) { return FASTID_ABI_VERSION; }
+
+// Diagnostics: subsequent tensor launches record, in CTA 0, kTrSlots clock64()
+// stamps per tile for the first `tiles` tiles into `device_buf` (null = off).
+extern "C" int fastid_debug_trace(long long* device_buf, int tiles) {
+    g_trace = device_buf;
+    g_trace_tiles = device_buf ? tiles : 0;
+    return FASTID_OK;
+}
+
+// Diagnostics: timing-experiment switches for subsequent launches (0 = normal).
+extern "C" int fastid_debug_flags(int flags) {
+    g_debug_flags = flags;
+    return FASTID_OK;
+}
 extern "C" const char* fastid_last_error(void) { return get_error(); }
 extern "C" int64_t fastid_row_stride(int64_t bit_length) { return bit_length > 0 ? row_stride_bytes(bit_length) : 0; }
 extern "C" int fastid_max_k(void) { return kMaxTopK; }

@@ -123,6 +123,20 @@ struct CompareArgs {
     uint32_t* hit_score;
     int64_t capacity;
     unsigned long long* hit_count;
+    // diagnostics (fastid_debug_trace): CTA 0 timestamps, or null
+    long long* trace;
+    int trace_tiles;
+    int debug_flags;  // bit 0: epilogue skips TMEM loads (timing experiments only)
+};
+
+// Per-tile trace slots written by CTA 0 when tracing is on (clock64 values).
+enum TraceSlot {
+    kTrMmaWait = 0,     // MMA warp starts waiting for the accumulator
+    kTrMmaGo = 1,       // ... accumulator free
+    kTrMmaIssued = 2,   // last MMA of the tile issued + committed
+    kTrEpi0 = 3,        // 16 slots: epilogue warp w acquired t_full (3 + w)
+    kTrRel0 = 19,       // 16 slots: epilogue warp w released t_empty (19 + w)
+    kTrSlots = 35
 };
 
 enum Mode { kFull = 0, kTopK = 1, kThreshold = 2 };

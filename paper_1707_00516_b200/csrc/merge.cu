@@ -3,15 +3,15 @@
 // lists of one device, and to fold the per-GPU lists after the NCCL gather
 // (the multi-GPU driver's only exchange).
 //
-// One warp per query: lane l owns lists l, l+32, ... (up to 16 per lane, so
-// n_lists <= 512); each of the k rounds takes the warp-wide minimum head and
+// One warp per query: lane l owns lists l, l+32, ... (up to 24 per lane, so
+// n_lists <= 768); each of the k rounds takes the warp-wide minimum head and
 // advances the winning list.
 #include "common.cuh"
 
 namespace fastid {
 namespace {
 
-constexpr int kMaxListsPerLane = 16;
+constexpr int kMaxListsPerLane = 24;
 
 __device__ __forceinline__ bool key_before(uint32_t s0, uint64_t i0, uint32_t s1, uint64_t i1) {
     return s0 < s1 || (s0 == s1 && i0 < i1);

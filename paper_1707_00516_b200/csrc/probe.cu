@@ -14,6 +14,7 @@ namespace fastid {
 namespace {
 
 // variant bit 0: accumulate every MMA into ONE accumulator (K-loop dependency)
+// variant bit 2: walk distinct operand addresses (A: 32 K-chunks, B: 20 chunks) like the real kernel
 // variant bit 1: warp 1 streams bulk copies (28 KB) from `src` into a 4-deep
 //                shared-memory ring while the MMAs run (operand-fill traffic)
 template <bool F4>
@@ -26,8 +27,10 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* 
     __shared__ __align__(8) uint64_t ring_empty[4];
     constexpr int BN = F4 ? 224 : 128;
     const int warp = threadIdx.x >> 5;
-    // zero operands: A 128 x 32 B, B BN x 32 B (one MMA's K)
-    for (int i = threadIdx.x; i < (128 + BN) * 32 / 16; i += blockDim.x)
+    // zero operands: A 128 x 32 B x 32 chunks (128 KB region reused), B BN x 32 B x 20 chunks
+    const bool walk = (variant & 4) != 0;
+    const int a_chunks = walk ? 32 : 1, b_chunks = walk ? 10 : 1;
+    for (int i = threadIdx.x; i < (walk ? 200 * 1024 : (128 + BN) * 32) / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     ptx::fence_proxy_async_smem();
     if (threadIdx.x == 0) {
@@ -54,10 +57,10 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* 
     ptx::tc_fence_after();
     if (threadIdx.x == 0) {
         const uint32_t a = ptx::smem_u32(smem);
-        const uint32_t b = a + 128 * 32;
-        const uint64_t ad = ptx::smem_desc(a, 128 * 16, 128);
-        const uint64_t bd = ptx::smem_desc(b, BN * 16, 128);
+        const uint32_t b = a + (walk ? 128 * 32 * 16 : 128 * 32);  // A region 64 KB when walking
         for (int i = 0; i < iters; ++i) {
+            const uint64_t ad = ptx::smem_desc(a + (uint32_t)((i % a_chunks) * 2 * 2048 % (64 * 1024)), 128 * 16, 128);
+            const uint64_t bd = ptx::smem_desc(b + (uint32_t)((i % b_chunks) * BN * 32), BN * 16, 128);
             const uint32_t d = tmem + (uint32_t)(((variant & 1) ? 0 : (i & 1)) * BN);
             if (F4)
                 ptx::mma_mxf4(d, ad, bd, ptx::idesc_mxf4(128, BN), tmem + 448, tmem + 480, i > 1);
@@ -122,10 +125,143 @@ __global__ void __launch_bounds__(256) popc_probe_kernel(int iters, uint32_t see
     if (s == 0xDEADBEEF) sink[0] = s;
 }
 
+// TMEM -> register read throughput: `warps` warps (4..16) each load `cols`
+// columns per tcgen05.ld.32x32b (x8/x16/x32/x64) `iters` times, one wait per load.
+template <int X>
+__global__ void __launch_bounds__(512, 1) tmem_read_probe_kernel(int iters, uint32_t* sink) {
+    __shared__ uint32_t tmem_slot;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) ptx::tmem_alloc(&tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 64);
+    uint32_t acc = 0;
+    for (int i = 0; i < iters; ++i) {
+        uint32_t v[64];
+        const uint32_t col = (uint32_t)((i * X) & 255);
+        if (X == 8) ptx::tmem_ld8(base + col, v);
+        if (X == 32) ptx::tmem_ld32(base + col, *reinterpret_cast<uint32_t(*)[32]>(v));
+        if (X == 64) {
+            ptx::tmem_ld32(base + col, *reinterpret_cast<uint32_t(*)[32]>(v));
+            ptx::tmem_ld32(base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        }
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < X; ++c) acc ^= v[c];
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+// MMA + TMEM-read contention: thread 0 issues `iters` mxf4 MMAs (M=128, N=224)
+// alternating accumulators at columns [0,448); warps 1..readers read columns
+// [0,448) with tcgen05.ld x32 until the MMAs finish.  sink[2*b] = TMEM bytes
+// read by CTA b, sink[2*b+1] = clock64 cycles the MMA stream took.
+__global__ void __launch_bounds__(512, 1) mma_tmem_contention_kernel(int iters, int readers,
+                                                                      unsigned long long* sink) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t done;
+    __shared__ volatile int stop;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < (128 + 224) * 32 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    ptx::fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&done, 1);
+        ptx::fence_mbar_init();
+        stop = 0;
+    }
+    if (warp == 0) ptx::tmem_alloc(&tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (warp < 4) {
+        const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+        ptx::tmem_fill32(lb + 448, 0x7F7F7F7Fu);
+        ptx::tmem_fill32(lb + 480, 0x7F7F7F7Fu);
+        ptx::tmem_wait_st();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (threadIdx.x == 0) {
+        const uint32_t a = ptx::smem_u32(smem);
+        const uint64_t ad = ptx::smem_desc(a, 128 * 16, 128);
+        const uint64_t bd = ptx::smem_desc(a + 128 * 32, 224 * 16, 128);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i)
+            ptx::mma_mxf4(tmem + (uint32_t)((i & 1) * 224), ad, bd, ptx::idesc_mxf4(128, 224), tmem + 448,
+                          tmem + 480, i > 1);
+        ptx::tc_commit(&done);
+        ptx::mbar_wait(&done, 0);
+        sink[2 * blockIdx.x + 1] = (unsigned long long)(clock64() - t0);
+        stop = 1;
+    } else if (warp >= 1 && warp <= readers) {
+        const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        unsigned long long bytes = 0;
+        uint32_t acc = 0;
+        int i = 0;
+        while (!stop) {
+            uint32_t v[32];
+            ptx::tmem_ld32(base + (uint32_t)((i * 32) % 448), v);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc ^= v[c];
+            bytes += 32 * 32 * 4;
+            ++i;
+        }
+        if (acc == 0x12345u) bytes += 1;
+        if ((threadIdx.x & 31) == 0) atomicAdd(&sink[2 * blockIdx.x], bytes);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
 }  // namespace
 }  // namespace fastid
 
 using namespace fastid;
+
+extern "C" int fastid_probe_contention(int iters, int readers, void* sink, void* stream) {
+    int dev = 0, sms = 148;
+    FASTID_CUDA(cudaGetDevice(&dev));
+    FASTID_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FASTID_CUDA(cudaFuncSetAttribute(mma_tmem_contention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+    mma_tmem_contention_kernel<<<sms, 512, 200 * 1024, (cudaStream_t)stream>>>(iters, readers,
+                                                                               (unsigned long long*)sink);
+    FASTID_LAUNCHED("mma_tmem_contention_kernel");
+    return FASTID_OK;
+}
+
+// Diagnostic: TMEM read probe.  Returns bytes read via *work.
+extern "C" int fastid_probe_tmem_read(int x, int warps, int iters, void* scratch, double* work, void* stream) {
+    int dev = 0, sms = 148;
+    FASTID_CUDA(cudaGetDevice(&dev));
+    FASTID_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (warps < 4 || warps > 16 || warps % 4) FASTID_FAIL(FASTID_E_INVALID, "warps must be 4, 8, 12 or 16");
+    if (x == 8) tmem_read_probe_kernel<8><<<sms, 32 * warps, 0, st>>>(iters, (uint32_t*)scratch);
+    else if (x == 32) tmem_read_probe_kernel<32><<<sms, 32 * warps, 0, st>>>(iters, (uint32_t*)scratch);
+    else if (x == 64) tmem_read_probe_kernel<64><<<sms, 32 * warps, 0, st>>>(iters, (uint32_t*)scratch);
+    else FASTID_FAIL(FASTID_E_INVALID, "x must be 8, 32 or 64");
+    FASTID_LAUNCHED("tmem_read_probe_kernel");
+    *work = (double)sms * warps * 32.0 * x * 4.0 * iters;
+    return FASTID_OK;
+}
 
 // Launch the probe for `formulation` with `iters` inner iterations per CTA (tensor)
 // or per thread (popc).  *work receives the bit-pairs (MACs) the launch performs.

@@ -47,7 +47,8 @@ constexpr int kFirstEpiWarp = 2 + kConvWarps;
 constexpr int kEpiWarps = 8;       // two per TMEM lane quadrant, splitting the columns
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kConvThreads + kEpiThreads;  // producer, MMA, converters, epilogue
-constexpr int kChunk = 16;         // accumulator columns per tcgen05.ld
+constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
+constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
 constexpr int kSmemLimit = 227 * 1024;
 
 template <int F>
@@ -119,27 +120,31 @@ __device__ __forceinline__ uint32_t decode_fast(uint32_t v) {
     return F == FASTID_TENSOR_F4 ? __float_as_uint(__uint_as_float(v) + 8388608.0f) - 0x4B000000u : v >> 7;
 }
 
-// Unsigned minimum of 16 values with 3-input mins (raw fp32 bits of
+// Unsigned minimum of 32 values with 3-input mins (raw fp32 bits of
 // non-negative floats order like the floats).
-__device__ __forceinline__ uint32_t min16(const uint32_t (&v)[16]) {
-    uint32_t a = __vimin3_u32(v[0], v[1], v[2]);
-    uint32_t b = __vimin3_u32(v[3], v[4], v[5]);
-    uint32_t c = __vimin3_u32(v[6], v[7], v[8]);
-    uint32_t d = __vimin3_u32(v[9], v[10], v[11]);
-    uint32_t e = __vimin3_u32(v[12], v[13], v[14]);
-    return __vimin3_u32(__vimin3_u32(a, b, c), __vimin3_u32(d, e, v[15]), 0xFFFFFFFFu);
+__device__ __forceinline__ uint32_t min32(const uint32_t (&v)[32]) {
+    uint32_t m[11];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) m[i] = __vimin3_u32(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    m[10] = __vimin3_u32(v[30], v[31], 0xFFFFFFFFu);
+    const uint32_t a = __vimin3_u32(m[0], m[1], m[2]);
+    const uint32_t b = __vimin3_u32(m[3], m[4], m[5]);
+    const uint32_t c = __vimin3_u32(m[6], m[7], m[8]);
+    return __vimin3_u32(__vimin3_u32(a, b, c), m[9], m[10]);
 }
 
-// v[c] for a run-time c without local memory: a 4-level select tree.
-__device__ __forceinline__ uint32_t pick16(const uint32_t (&v)[16], int c) {
-    uint32_t a[8], b[4], d[2];
+// v[c] for a run-time c without local memory: a 5-level select tree.
+__device__ __forceinline__ uint32_t pick32(const uint32_t (&v)[32], int c) {
+    uint32_t a[16], b[8], d[4], e[2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = (c & 8) ? v[i + 8] : v[i];
+    for (int i = 0; i < 16; ++i) a[i] = (c & 16) ? v[i + 16] : v[i];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) b[i] = (c & 4) ? a[i + 4] : a[i];
+    for (int i = 0; i < 8; ++i) b[i] = (c & 8) ? a[i + 8] : a[i];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) d[i] = (c & 2) ? b[i + 2] : b[i];
-    return (c & 1) ? d[1] : d[0];
+    for (int i = 0; i < 4; ++i) d[i] = (c & 4) ? b[i + 4] : b[i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) e[i] = (c & 2) ? d[i + 2] : d[i];
+    return (c & 1) ? e[1] : e[0];
 }
 
 // Position in a ring of mbarrier-guarded stages: slot index + phase parity.
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&t_full[i], 1);
-            ptx::mbar_init(&t_empty[i], kEpiThreads);
+            ptx::mbar_init(&t_empty[i], IMG ? kEpiThreads + kConvThreads : kEpiThreads);
         }
         ptx::mbar_init(a_full, kConvThreads);
         for (int i = 0; i < kMaxAStages; ++i) {
@@ -320,15 +325,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer (one thread) ----------------
         if (lane == 0) {
             constexpr uint32_t idesc = F == FASTID_TENSOR_F4 ? ptx::idesc_mxf4(kM, BN) : ptx::idesc_i8(kM, BN);
-            const uint32_t a_base = ptx::smem_u32(sA);
-            const uint32_t u_base = ptx::smem_u32(sU);
+            const uint64_t a_desc0 = ptx::smem_desc(ptx::smem_u32(sA), kM * 16, 128);
+            const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(sU), BN * 16, 128);
             if (!SA) ptx::mbar_wait(a_full, 0);
             ptx::tc_fence_after();
             Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
             for (int64_t t = t_begin; t < t_end; ++t, ++local) {
                 const int acc = local & 1;
+                const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles;
+                if (tr) a.trace[local * kTrSlots + kTrMmaWait] = clock64();
                 ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
+                if (tr) a.trace[local * kTrSlots + kTrMmaGo] = clock64();
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 for (int ks = 0; ks < n_kst; ++ks, ru.next()) {
@@ -337,19 +345,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
                     ptx::mbar_wait(&u_full[s], ru.phase);
                     ptx::tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < Fmt<F>::kMmaPerStage; ++kk) {
-                        const uint32_t acol = SA ? (uint32_t)(2 * kk) : (uint32_t)(ks * kWordsPerStage * CPW + 2 * kk);
-                        const uint32_t abase = SA ? a_base + (uint32_t)(sa * AB) : a_base;
-                        const uint64_t ad = ptx::smem_desc(abase + acol * (kM * 16), kM * 16, 128);
-                        const uint64_t bd =
-                            ptx::smem_desc(u_base + s * UB + (uint32_t)(2 * kk) * (BN * 16), BN * 16, 128);
-                        const uint32_t accum = (ks | kk) ? 1u : 0u;
-                        if (F == FASTID_TENSOR_F4)
-                            ptx::mma_mxf4(d, ad, bd, idesc, tmem + kSfaCol, tmem + kSfbCol, accum);
-                        else
-                            ptx::mma_i8(d, ad, bd, idesc, accum);
-                    }
+                    // descriptors of this stage's first K-step; later steps add fixed strides
+                    const uint32_t a_off = SA ? (uint32_t)(sa * AB) : (uint32_t)(ks * kWordsPerStage * CPW) * (kM * 16);
+                    const uint64_t ad = a_desc0 + (uint64_t)(a_off >> 4);
+                    const uint64_t bd = b_desc0 + (uint64_t)(((uint32_t)s * UB) >> 4);
+                    const uint64_t a_step = (2 * kM * 16) >> 4, b_step = (2 * BN * 16) >> 4;
+                    if (F == FASTID_TENSOR_F4)
+                        ptx::mma_mxf4_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol, tmem + kSfbCol,
+                                             ks ? 1u : 0u);
+                    else
+                        ptx::mma_i8_stage8(d, ad, bd, a_step, b_step, idesc, ks ? 1u : 0u);
                     ptx::tc_commit(&u_empty[s]);  // stage s reusable once these MMAs retire
                     if (SA) {
                         ptx::tc_commit(&ar_empty[sa]);
@@ -357,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
+                if (tr) a.trace[local * kTrSlots + kTrMmaIssued] = clock64();
             }
         }
     } else if (warp < kFirstEpiWarp) {
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(a_full);
         }
-        if (IMG) goto converters_done;
+        if (IMG) goto epilogue;
         {
         // Work unit = (known row, 16-byte half of the stage): 2*BN units per stage.
         constexpr int kUnits = 2 * BN;
@@ -442,17 +448,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         }
-    converters_done:;
-    } else {
+    }
+    if (warp >= kFirstEpiWarp || (IMG && warp >= 2)) {
+    epilogue:;
         // ---------------- epilogue: one unknown per thread ----------------
-        // Warp w reads TMEM lanes 32*(w%4).. (its quadrant) and one half of the
-        // accumulator columns; scores stay as raw accumulator bits (fp32 of an
-        // exact integer is order-preserving as u32), so the hot loop is compares
-        // only and the rare candidates take a warp-uniform slow path.
-        const int ew = warp - kFirstEpiWarp;
+        // A warp reads TMEM lanes 32*(w%4).. (its quadrant) and 1/n_splits of the
+        // accumulator columns, in batches of up to 32 columns (x8 loads, one
+        // wait per batch).  Scores stay raw accumulator bits (fp32 of an exact
+        // integer orders like u32), so the hot path is a 3-input-min tree and
+        // one compare per batch; candidates take a rare per-lane slow path.
+        constexpr int kSplitsMain = kEpiWarps / 4;                       // 2
+        constexpr int kSplits = IMG ? (kEpiWarps + kConvWarps) / 4 : kSplitsMain;  // 4 with an image
+        static_assert(kSplits <= kMaxSplits, "split count");
+        constexpr int kCols = BN / kSplits;  // 112 / 56 (mxf4), 64 / 32 (i8)
+        static_assert(kCols % 8 == 0, "columns per split must be a multiple of 8");
+        const int ew = IMG ? (warp >= kFirstEpiWarp ? warp - kFirstEpiWarp + kConvWarps : warp - 2) : warp - kFirstEpiWarp;
         const int quad = warp & 3;
-        const int half = ew >> 2;
-        constexpr int kHalfCols = BN / 2;  // 112 (mxf4) or 64 (i8): a multiple of kChunk
+        const int split = ew >> 2;
         const int m = quad * 32 + lane;
         const int64_t q = q0 + m;
         const bool q_ok = q < a.n_queries;
@@ -467,46 +479,72 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t t = t_begin; t < t_end; ++t, ++local) {
             const int acc = local & 1;
             ptx::mbar_wait(&t_full[acc], (local >> 1) & 1);
+            const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
+            if (tr) a.trace[local * kTrSlots + kTrEpi0 + ew] = clock64();
             ptx::tc_fence_after();
-            const int64_t r0 = t * BN + half * kHalfCols;
+            const int64_t r0 = t * BN + split * kCols;
             const int64_t rows_left = a.n_refs - r0;
-            // rows of this half that exist (0 for padding unknowns); full tiles skip masking
-            const int rl = !q_ok ? 0 : (rows_left >= kHalfCols ? kHalfCols : (rows_left > 0 ? (int)rows_left : 0));
-            const bool full = rl == kHalfCols;
+            const int rl = !q_ok ? 0 : (rows_left >= kCols ? kCols : (rows_left > 0 ? (int)rows_left : 0));
+            const bool full = rl == kCols;
+            const uint32_t col_base = (uint32_t)(acc * BN + split * kCols);
 #pragma unroll 1
-            for (int ch = 0; ch < kHalfCols / kChunk; ++ch) {
-                uint32_t v[kChunk];
-                ptx::tmem_ld16(lane_base + (uint32_t)(acc * BN + half * kHalfCols + ch * kChunk), v);
-                ptx::tmem_wait_ld();
-                if (ch + 1 == kHalfCols / kChunk) {
-                    // this warp's half of the accumulator is in registers: release it
+            for (int b0 = 0; b0 < kCols; b0 += kBatch) {
+                const int nb = kCols - b0 < kBatch ? kCols - b0 : kBatch;  // multiple of 8, warp-uniform
+                uint32_t v[kBatch];
+                if (!(a.debug_flags & 1)) {
+                    // widest loads that fit (x32 moves ~40% more TMEM bytes/clk than x8)
+                    const uint32_t ta = lane_base + col_base + (uint32_t)b0;
+                    if (nb == 32) {
+                        ptx::tmem_ld32(ta, v);
+                    } else {
+                        int o = 0;
+                        if (nb - o >= 16) {
+                            ptx::tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                            o = 16;
+                        }
+                        if (nb - o >= 8) {
+                            ptx::tmem_ld8(ta + (uint32_t)o, &v[o]);
+                            o += 8;
+                        }
+                        if (nb - o >= 8) ptx::tmem_ld8(ta + (uint32_t)o, &v[o]);
+                    }
+                    ptx::tmem_wait_ld();
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kBatch; ++c) v[c] = 0xFFFFFFFFu;
+                }
+                if (b0 + kBatch >= kCols) {
+                    // this warp's columns are all in registers: release the accumulator
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(&t_empty[acc]);
+                    if (tr) a.trace[local * kTrSlots + kTrRel0 + ew] = clock64();
                 }
-                const int64_t rc = r0 + ch * kChunk;
-                const int left = rl - ch * kChunk;
-                const uint32_t valid =
-                    full || left >= kChunk ? 0xFFFFu : (left <= 0 ? 0u : (1u << left) - 1u);
+                const int left = rl - b0;
+                const uint32_t valid = full || left >= kBatch ? (nb == 32 ? 0xFFFFFFFFu : (1u << nb) - 1u)
+                                                              : (left <= 0 ? 0u : (1u << left) - 1u);
+                const int64_t rc = r0 + b0;
                 if (MODE == kFull) {
 #pragma unroll
-                    for (int c = 0; c < kChunk; ++c)
-                        if (full || ((valid >> c) & 1u)) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
-                } else if (MODE == kTopK) {
-                    // common case: one min over the chunk, one compare (3-input mins)
-                    if (!full && valid != 0xFFFFu) {
+                    for (int c = 0; c < kBatch; ++c)
+                        if ((valid >> c) & 1u) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
+                    continue;
+                }
+                if (valid != 0xFFFFFFFFu) {
 #pragma unroll
-                        for (int c = 0; c < kChunk; ++c)
-                            if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
-                    }
-                    if (min16(v) < thr_bits) {
+                    for (int c = 0; c < kBatch; ++c)
+                        if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
+                }
+                const uint32_t mn = min32(v);
+                if (MODE == kTopK) {
+                    if (mn < thr_bits) {
                         uint32_t cand = 0;
 #pragma unroll
-                        for (int c = 0; c < kChunk; ++c) cand |= (v[c] < thr_bits ? 1u : 0u) << c;
+                        for (int c = 0; c < kBatch; ++c) cand |= (v[c] < thr_bits ? 1u : 0u) << c;
                         // rare: one insertion per loop trip, value picked by a select tree
                         while (cand) {
                             const int c = __ffs(cand) - 1;
                             cand &= cand - 1;
-                            const uint32_t vc = pick16(v, c);
+                            const uint32_t vc = pick32(v, c);
                             if (vc < thr_bits) {
                                 top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
                                 const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
@@ -515,31 +553,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else {
-                    if (!full && valid != 0xFFFFu) {
-#pragma unroll
-                        for (int c = 0; c < kChunk; ++c)
-                            if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
-                    }
-                    const bool any = min16(v) <= hit_bits;
                     uint32_t hit = 0;
-                    if (any) {
+                    if (mn <= hit_bits) {
 #pragma unroll
-                        for (int c = 0; c < kChunk; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
+                        for (int c = 0; c < kBatch; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
                     }
                     if (__any_sync(0xffffffffu, hit != 0)) {
                         uint32_t all = __reduce_or_sync(0xffffffffu, hit);
                         while (all) {  // warp-uniform walk over columns with a hit in any lane
                             const int c = __ffs(all) - 1;
                             all &= all - 1;
-                            emit_hits(a, (hit >> c) & 1u, (uint32_t)q, rc + c, decode_exact<F>(pick16(v, c)));
+                            emit_hits(a, (hit >> c) & 1u, (uint32_t)q, rc + c, decode_exact<F>(pick32(v, c)));
                         }
                     }
                 }
             }
         }
         if (MODE == kTopK && q_ok) {
-            const int64_t off = (((int64_t)slice * 2 + half) * a.n_queries + q) * KP;
+            const int64_t off = (((int64_t)slice * kMaxSplits + split) * a.n_queries + q) * KP;
             top.store(a.part_scores + off, a.part_index + off, a.ref_base);
+        }
+        if (MODE == kTopK && q_ok && split == 0) {
+            // unused split slots of this slice hold empty lists (the merge skips them)
+            for (int s2 = kSplits; s2 < kMaxSplits; ++s2) {
+                const int64_t off2 = (((int64_t)slice * kMaxSplits + s2) * a.n_queries + q) * KP;
+                TopList<KP> empty;
+                empty.clear();
+                empty.store(a.part_scores + off2, a.part_index + off2, a.ref_base);
+            }
         }
     }
 
@@ -733,7 +774,7 @@ int launch_fmt(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t strea
     const int slices = slices_for<F>(a.n_refs, a.n_queries);
     if (mode == kFull) return launch_one<F, kFull, 1>(a, slices, stream);
     if (mode == kThreshold) return launch_one<F, kThreshold, 1>(a, slices, stream);
-    *n_parts = 2 * slices;  // one partial list per (slice, epilogue column half)
+    *n_parts = kMaxSplits * slices;  // one partial list per (slice, epilogue column split)
     switch (a.kpad) {
         case 8: return launch_one<F, kTopK, 8>(a, slices, stream);
         case 16: return launch_one<F, kTopK, 16>(a, slices, stream);
@@ -767,8 +808,8 @@ int build_tensor_image(const CompareArgs& a, int formulation, void* image, cudaS
 }
 
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation) {
-    if (formulation == FASTID_TENSOR_I8) return 2 * slices_for<FASTID_TENSOR_I8>(n_refs, n_queries);
-    return 2 * slices_for<FASTID_TENSOR_F4>(n_refs, n_queries);
+    if (formulation == FASTID_TENSOR_I8) return kMaxSplits * slices_for<FASTID_TENSOR_I8>(n_refs, n_queries);
+    return kMaxSplits * slices_for<FASTID_TENSOR_F4>(n_refs, n_queries);
 }
 
 int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream) {

@@ -106,6 +106,59 @@ __device__ __forceinline__ void mma_mxf4(uint32_t tmem_d, uint64_t adesc, uint64
         : "memory");
 }
 
+// One pipeline stage of MMAs in a single asm block: N consecutive K-steps,
+// operand descriptors advanced by fixed 16-byte-unit strides (a_step/b_step),
+// the first step accumulating only when `accumulate` is set.  Issuing the whole
+// stage at once keeps the single-thread issue path to a few instructions per
+// MMA (the stage's MMAs otherwise cost ~20 uniform-datapath ops each).
+__device__ __forceinline__ void mma_mxf4_stage4(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint64_t a_step,
+                                                uint64_t b_step, uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                                uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, t;\n"
+        ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.u32 t, 0, 0;\n"
+        "add.s64 a1, %1, %7; add.s64 b1, %2, %8;\n"
+        "add.s64 a2, a1, %7; add.s64 b2, b1, %8;\n"
+        "add.s64 a3, a2, %7; add.s64 b3, b2, %8;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a1, b1, %3, [%5], [%6], t;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a2, b2, %3, [%5], [%6], t;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a3, b3, %3, [%5], [%6], t;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb), "l"(a_step), "l"(b_step)
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8_stage8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint64_t a_step,
+                                              uint64_t b_step, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, t;\n"
+        ".reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.u32 t, 0, 0;\n"
+        "add.s64 a1, %1, %5; add.s64 b1, %2, %6;\n"
+        "add.s64 a2, a1, %5; add.s64 b2, b1, %6;\n"
+        "add.s64 a3, a2, %5; add.s64 b3, b2, %6;\n"
+        "add.s64 a4, a3, %5; add.s64 b4, b3, %6;\n"
+        "add.s64 a5, a4, %5; add.s64 b5, b4, %6;\n"
+        "add.s64 a6, a5, %5; add.s64 b6, b5, %6;\n"
+        "add.s64 a7, a6, %5; add.s64 b7, b6, %6;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, t;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, t;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, t;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a4, b4, %3, t;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a5, b5, %3, t;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a6, b6, %3, t;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], a7, b7, %3, t;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "l"(a_step), "l"(b_step)
+        : "memory");
+}
+
 // 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread (lane = thread).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
@@ -125,6 +178,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
+}
+// 32 lanes x 8 columns into v[0..7].
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
