@@ -136,7 +136,9 @@ enum TraceSlot {
     kTrMmaIssued = 2,   // last MMA of the tile issued + committed
     kTrEpi0 = 3,        // 16 slots: epilogue warp w acquired t_full (3 + w)
     kTrRel0 = 19,       // 16 slots: epilogue warp w released t_empty (19 + w)
-    kTrSlots = 35
+    kTrB0Loaded = 35,   // 16 slots: batch 0 in registers
+    kTrB0Done = 51,     // 16 slots: batch 0 processed
+    kTrSlots = 67
 };
 
 enum Mode { kFull = 0, kTopK = 1, kThreshold = 2 };

@@ -43,10 +43,14 @@ constexpr int kMaxUnpackedStages = 6;
 constexpr int kMaxAStages = 4;
 constexpr int kConvWarps = 8;      // two per SMSP: halves the per-stage unpack latency
 constexpr int kConvThreads = 32 * kConvWarps;
-constexpr int kFirstEpiWarp = 2 + kConvWarps;
+// Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
+// highest warp ids (the scheduler favours higher ids), converters the lowest.
+constexpr int kFirstEpiWarp = kConvWarps;
 constexpr int kEpiWarps = 8;       // two per TMEM lane quadrant, splitting the columns
 constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kThreads = 64 + kConvThreads + kEpiThreads;  // producer, MMA, converters, epilogue
+constexpr int kProducerWarp = kConvWarps + kEpiWarps;
+constexpr int kMmaWarp = kProducerWarp + 1;
+constexpr int kThreads = kConvThreads + kEpiThreads + 64;  // converters, epilogue, producer, MMA
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
 constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
 constexpr int kSmemLimit = 227 * 1024;
@@ -274,13 +278,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap);
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, Fmt<F>::kTmemCols);
+    if (warp == kProducerWarp && lane == 0) ptx::prefetch_tmap(&tmap);
+    if (warp == kMmaWarp) ptx::tmem_alloc(tmem_slot, Fmt<F>::kTmemCols);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (F == FASTID_TENSOR_F4 && warp >= kFirstEpiWarp) {
+    if (F == FASTID_TENSOR_F4 && warp >= kFirstEpiWarp && warp < kProducerWarp) {
         // unit block scales (ue8m0 127) for every MMA: whole SF region, all lanes
         const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         ptx::tmem_fill32(lb + kSfaCol, kUnitScales);
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
 
-    if (warp == 0) {
+    if (warp == kProducerWarp) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
             Ring ra(SA ? lay.sa : 1), rp(SP > 0 ? SP : 1), ru(SU);
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer (one thread) ----------------
         if (lane == 0) {
             constexpr uint32_t idesc = F == FASTID_TENSOR_F4 ? ptx::idesc_mxf4(kM, BN) : ptx::idesc_i8(kM, BN);
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp < kFirstEpiWarp) {
         // ---------------- converters ----------------
-        const int ct = threadIdx.x - 64;  // 0..kConvThreads-1
+        const int ct = threadIdx.x;  // 0..kConvThreads-1
         {
             // Resident A = complemented unknown rows; zero past the row.  Threads
             // 0..127 each build one row.
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         }
     }
-    if (warp >= kFirstEpiWarp || (IMG && warp >= 2)) {
+    if (warp < kProducerWarp && (warp >= kFirstEpiWarp || IMG)) {
     epilogue:;
         // ---------------- epilogue: one unknown per thread ----------------
         // A warp reads TMEM lanes 32*(w%4).. (its quadrant) and 1/n_splits of the
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         static_assert(kSplits <= kMaxSplits, "split count");
         constexpr int kCols = BN / kSplits;  // 112 / 56 (mxf4), 64 / 32 (i8)
         static_assert(kCols % 8 == 0, "columns per split must be a multiple of 8");
-        const int ew = IMG ? (warp >= kFirstEpiWarp ? warp - kFirstEpiWarp + kConvWarps : warp - 2) : warp - kFirstEpiWarp;
+        const int ew = IMG ? warp : warp - kFirstEpiWarp;
         const int quad = warp & 3;
         const int split = ew >> 2;
         const int m = quad * 32 + lane;
@@ -487,8 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int rl = !q_ok ? 0 : (rows_left >= kCols ? kCols : (rows_left > 0 ? (int)rows_left : 0));
             const bool full = rl == kCols;
             const uint32_t col_base = (uint32_t)(acc * BN + split * kCols);
-#pragma unroll 1
+#pragma unroll
             for (int b0 = 0; b0 < kCols; b0 += kBatch) {
+                if (tr && b0 == kBatch) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
                 const int nb = kCols - b0 < kBatch ? kCols - b0 : kBatch;  // multiple of 8, warp-uniform
                 uint32_t v[kBatch];
                 if (!(a.debug_flags & 1)) {
@@ -513,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < kBatch; ++c) v[c] = 0xFFFFFFFFu;
                 }
+                if (tr && b0 == 0) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 if (b0 + kBatch >= kCols) {
                     // this warp's columns are all in registers: release the accumulator
                     ptx::tc_fence_before();
@@ -586,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, Fmt<F>::kTmemCols);
     }

@@ -14,7 +14,7 @@ q = torch.randint(-2**62, 2**62, (n_q, L // 64), dtype=torch.int64, device="cuda
 db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation="tensor_f4")
 dq = m.DevicePanel.from_words(q, L)
 db.topk_device(dq, 16); torch.cuda.synchronize()
-buf = torch.zeros((tiles, 35), dtype=torch.int64, device="cuda")
+buf = torch.zeros((tiles, 67), dtype=torch.int64, device="cuda")
 _native.lib().fastid_debug_trace(buf.data_ptr(), tiles)
 db.topk_device(dq, 16); torch.cuda.synchronize()
 _native.lib().fastid_debug_trace(None, 0)
@@ -30,6 +30,13 @@ print("median MMA tile period (cycles):", np.median(d[d > 0]) if len(d) else Non
 print("median MMA wait (go - wait):", np.median(t[:, 1] - t[:, 0]))
 print("median epilogue span (max rel - min acq):", np.median(t[:, 19:35].max(1) - t[:, 3:19].min(1)))
 print("median lag commit->epi acquire:", np.median(t[:, 3:19].min(1) - t[:, 2]))
+acq, b0l, b0d, rel = t[:, 3:19], t[:, 35:51], t[:, 51:67], t[:, 19:35]
+sl = slice(200, None)
+print("per-warp medians (cycles) over tiles 200..:")
+print("  acquire -> batch0 loaded:", np.median((b0l - acq)[sl], axis=0).astype(int).tolist())
+print("  batch0 loaded -> processed:", np.median((b0d - b0l)[sl], axis=0).astype(int).tolist())
+print("  batch0 processed -> release (batch1 loaded):", np.median((rel - b0d)[sl], axis=0).astype(int).tolist())
+print("  acquire spread (max-min):", int(np.median((acq.max(1) - acq.min(1))[sl])))
 
 # same run with the epilogue's TMEM loads switched off (results invalid; timing only)
 _native.lib().fastid_debug_flags(1)
