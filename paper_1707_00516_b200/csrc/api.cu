@@ -244,8 +244,8 @@ int topk_partials_impl(const void* refs, const void* image, int64_t n_refs, cons
     a.part_scores = (uint32_t*)(a.part_index + (size_t)parts * n_queries * kp);
     int launched_parts = 0;
     if (int rc = launch(kTopK, a, f, &launched_parts, (cudaStream_t)stream)) return rc;
-    if (launched_parts != parts) FASTID_FAIL(FASTID_E_INVALID, "internal: partition mismatch");
-    *n_lists = parts;
+    if (launched_parts > parts) FASTID_FAIL(FASTID_E_INVALID, "internal: partition mismatch");
+    *n_lists = launched_parts;
     *list_len = kp;
     *index_offset = (size_t)((uintptr_t)a.part_index - (uintptr_t)workspace);
     *score_offset = (size_t)((uintptr_t)a.part_scores - (uintptr_t)workspace);

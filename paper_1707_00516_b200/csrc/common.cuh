@@ -126,7 +126,7 @@ struct CompareArgs {
     // diagnostics (fastid_debug_trace): CTA 0 timestamps, or null
     long long* trace;
     int trace_tiles;
-    int debug_flags;  // bit 0: epilogue skips TMEM loads (timing experiments only)
+    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 1: no CTA pairs; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits (timing experiments only)
 };
 
 // Per-tile trace slots written by CTA 0 when tracing is on (clock64 values).

@@ -103,6 +103,96 @@ __global__ void __launch_bounds__(128, 1) mma_probe_kernel(int iters, uint32_t* 
     }
 }
 
+// CTA-pair variant: the leader issues cta_group::2 mxf4 MMAs (M = 256, N = BN)
+// on resident operands (each CTA holds 128 A rows and BN/2 B rows); `walk`
+// steps the operand addresses through distinct K-chunks like the real kernel.
+template <int BN>
+__global__ void __launch_bounds__(128, 1) mma_pair_probe_kernel(int iters, uint32_t* sink, int walk) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t done;
+    __shared__ __align__(8) uint64_t sink_bar[8];
+    __shared__ __align__(8) uint64_t open_bar;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t rank = ptx::cluster_ctarank();
+    for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x) {
+        // walk & 4: random 0/1 operands (e2m1 nibbles 0x0 / 0x2) like real profiles
+        uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x * 97u;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (walk & 4) {
+            h ^= h >> 13; h *= 0x5bd1e995u; v.x = (h & 0x11111111u) << 1;
+            h ^= h >> 15; h *= 0x5bd1e995u; v.y = (h & 0x11111111u) << 1;
+            h ^= h >> 13; h *= 0x5bd1e995u; v.z = (h & 0x11111111u) << 1;
+            h ^= h >> 15; h *= 0x5bd1e995u; v.w = (h & 0x11111111u) << 1;
+        }
+        reinterpret_cast<uint4*>(smem)[i] = v;
+    }
+    ptx::fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&done, 1);
+        for (int i = 0; i < 8; ++i) ptx::mbar_init(&sink_bar[i], 1);
+        ptx::mbar_init(&open_bar, 1);
+        ptx::mbar_arrive(&open_bar);  // phase 0 complete: waits on parity 0 pass at once
+        ptx::fence_mbar_init();
+    }
+    ptx::cluster_sync();
+    if (warp == 0) ptx::tmem_alloc_pair(&tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    {
+        const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+        ptx::tmem_fill32(lb + 448, 0x7F7F7F7Fu);
+        ptx::tmem_fill32(lb + 480, 0x7F7F7F7Fu);
+        ptx::tmem_wait_st();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    if (threadIdx.x == 0 && rank == 0) {
+        const uint32_t a = ptx::smem_u32(smem);
+        const uint32_t b = a + 64 * 1024;
+        const int chunks = walk ? 16 : 1;
+        for (int i = 0; i < iters; ++i) {
+            // walk & 32: a (satisfied) mbarrier wait + tcgen05 fence before every 4 MMAs
+            if ((walk & 32) && (i & 3) == 0) {
+                ptx::mbar_wait(&open_bar, 0);
+                ptx::tc_fence_after();
+            }
+            const int c = i % chunks;
+            const uint64_t ad = ptx::smem_desc(a + (uint32_t)(c * 4096), 128 * 16, 128);
+            const uint64_t bd = ptx::smem_desc(b + (uint32_t)(c * (BN / 2) * 32), (BN / 2) * 16, 128);
+            // walk & 16: the real kernel's tile structure -- 16 K-steps into one of two
+            // accumulators at column offset 0 / BN, the first step of a tile overwriting
+            const bool tiled = (walk & 16) != 0;
+            const uint32_t d = tmem + (uint32_t)(tiled ? ((i >> 4) & 1) * BN
+                                                       : ((walk & 2) ? 0 : (i & 1) * (BN <= 224 ? 224 : 256)));
+            const uint32_t accf = tiled ? (uint32_t)((i & 15) != 0) : (uint32_t)(i > 1);
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d),
+                "l"(ad), "l"(bd), "r"(ptx::idesc_mxf4(256, BN)), "r"(accf), "r"(tmem + 448),
+                "r"(tmem + 480)
+                : "memory");
+            // walk & 8: commit (multicast) after every 4 MMAs like the real kernel's stages
+            if ((walk & 8) && (i & 3) == 3) ptx::tc_commit_pair(&sink_bar[(i >> 2) & 7], 0x3);
+        }
+        ptx::tc_commit_pair(&done, 0x3);
+    }
+    if (threadIdx.x == 0) ptx::mbar_wait(&done, 0);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        uint32_t v[32];
+        ptx::tmem_ld32(tmem, v);
+        ptx::tmem_wait_ld();
+        if (threadIdx.x == 0) sink[blockIdx.x] = v[0];
+        ptx::tmem_dealloc_pair(tmem, 512);
+    }
+}
+
 __global__ void __launch_bounds__(256) popc_probe_kernel(int iters, uint32_t seed, uint32_t* sink) {
     uint32_t r[8], acc[16];
 #pragma unroll
@@ -287,6 +377,31 @@ extern "C" int fastid_probe_variant(int formulation, int variant, int iters, voi
         return FASTID_OK;
     }
     const bool f4 = formulation == FASTID_TENSOR_F4 || formulation == FASTID_AUTO;
+    if (f4 && (variant & 8)) {
+        // CTA pairs: variant bit 4 selects N = 256 (else 224), bit 2 walks operand addresses
+        const bool n256 = (variant & 16) != 0;
+        const bool n192 = (variant & 128) != 0;
+        auto kern = n192 ? mma_pair_probe_kernel<192> : (n256 ? mma_pair_probe_kernel<256> : mma_pair_probe_kernel<224>);
+        FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(sms & ~1));
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = 160 * 1024;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // variant bit 0: one accumulator (K-loop dependency chain), bit 2: walk operand addresses
+        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, iters, sink, ((variant & 4) ? 1 : 0) | ((variant & 1) ? 2 : 0) | ((variant & 32) ? 4 : 0) |
+                                                             ((variant & 64) ? 8 : 0) | ((variant & 256) ? 16 : 0) | ((variant & 512) ? 32 : 0)));
+        FASTID_LAUNCHED("mma_pair_probe_kernel");
+        *work = (double)(sms / 2) * iters * 256.0 * (n192 ? 192 : (n256 ? 256 : 224)) * 64.0;
+        return FASTID_OK;
+    }
     const int bn = f4 ? 224 : 128;
     const int smem = (128 + bn) * 32;
     if (f4) {

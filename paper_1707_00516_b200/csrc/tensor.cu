@@ -39,18 +39,25 @@ constexpr int kStageBytesPacked = 32;  // packed bytes per known row per stage (
 constexpr int kWordsPerStage = kStageBytesPacked / 4;
 constexpr int kMaxPackedStages = 12;
 constexpr int kMinPackedStages = 4;
-constexpr int kMaxUnpackedStages = 6;
+constexpr int kMaxUnpackedStages = 8;
 constexpr int kMaxAStages = 4;
-constexpr int kConvWarps = 8;      // two per SMSP: halves the per-stage unpack latency
-constexpr int kConvThreads = 32 * kConvWarps;
 // Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
 // highest warp ids (the scheduler favours higher ids), converters the lowest.
-constexpr int kFirstEpiWarp = kConvWarps;
-constexpr int kEpiWarps = 8;       // two per TMEM lane quadrant, splitting the columns
-constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kProducerWarp = kConvWarps + kEpiWarps;
-constexpr int kMmaWarp = kProducerWarp + 1;
-constexpr int kThreads = kConvThreads + kEpiThreads + 64;  // converters, epilogue, producer, MMA
+// Packed operands: 8 converter warps (two per SMSP) + 8 epilogue warps.  A
+// prepared image needs no converters: the epilogue gets 12 warps (mxf4, three
+// column splits of 64) or 16 (i8, four of 32) -- at 14 warps per CTA no SMSP
+// holds more than 4, which leaves 128 registers per thread for the epilogue
+// to hold all of its accumulator columns at once.
+template <int F, bool IMG>
+struct Roles {
+    static constexpr int kConvWarps = IMG ? 0 : 8;
+    static constexpr int kEpiWarps = IMG ? (F == FASTID_TENSOR_F4 ? 12 : 16) : 8;
+    static constexpr int kBuildWarps = IMG ? 4 : kConvWarps;  // build the resident A tile
+    static constexpr int kFirstEpiWarp = kConvWarps;
+    static constexpr int kProducerWarp = kConvWarps + kEpiWarps;
+    static constexpr int kMmaWarp = kProducerWarp + 1;
+    static constexpr int kThreads = 32 * (kMmaWarp + 1);
+};
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
 constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
 constexpr int kSmemLimit = 227 * 1024;
@@ -61,15 +68,13 @@ template <>
 struct Fmt<FASTID_TENSOR_I8> {
     static constexpr int BN = 128;          // knowns per tile (MMA N)
     static constexpr int kCoresPerWord = 2; // 16-B core columns produced per packed u32
-    static constexpr int kMmaPerStage = 8;  // K = 32 B of operand per MMA
     static constexpr int kTmemCols = 256;   // 2 x BN accumulator columns
 };
 template <>
 struct Fmt<FASTID_TENSOR_F4> {
-    static constexpr int BN = 224;
+    static constexpr int BN = 192;          // 3 epilogue splits of 64 columns; pairs stream 96 rows each
     static constexpr int kCoresPerWord = 1;
-    static constexpr int kMmaPerStage = 4;
-    static constexpr int kTmemCols = 512;   // 2 x 224 accumulators + 64 scale-factor columns
+    static constexpr int kTmemCols = 512;   // 2 x 192 accumulators + 64 scale-factor columns (448..511)
 };
 
 constexpr uint32_t kSfaCol = 448;  // mxf4: unit scale factors for A (32 columns)
@@ -177,16 +182,20 @@ struct Layout {
     static constexpr int kPackedStageBytes = BN * kStageBytesPacked;
     static constexpr int kAStageBytes = kM * 16 * kWordsPerStage * Fmt<F>::kCoresPerWord;
     static constexpr int kBarBytes = 8 * (2 * kMaxPackedStages + 2 * kMaxUnpackedStages + 2 * kMaxAStages + 5) + 16;
+    // top-k: each epilogue split's published admission bound per unknown (u32 raw score bits)
+    static constexpr int kPubBytes = kMaxSplits * kM * 4;
     int n_kst;    // stages per tile (K padded to 256 loci)
     int a_bytes;  // resident A tile, or the A ring when streaming
     int sa;       // A ring depth (streamed A only)
     int su;       // operand ring depth (converter or TMA -> MMA)
     int sp;       // packed ring depth (TMA -> converter); 0 with a tensor image
     bool img;
+    int ub;       // operand-ring stage bytes: the whole tile, or this CTA's half of it in a pair
     int off_u, off_p, off_bar, total;
-    __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false) {
+    __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false, bool pair = false) {
         n_kst = (int)((stride + kStageBytesPacked - 1) / kStageBytesPacked);
         img = image;
+        ub = pair ? kUnpackedStageBytes / 2 : kUnpackedStageBytes;
         sa = 0;
         if (!stream_a) {
             a_bytes = n_kst * kAStageBytes;
@@ -200,10 +209,10 @@ struct Layout {
         }
     }
     __host__ __device__ void place() {
-        const int room = kSmemLimit - a_bytes - kBarBytes;
+        const int room = kSmemLimit - a_bytes - kBarBytes - kPubBytes;
         if (img) {
             // the tensor image is already in the UMMA layout: only the operand ring
-            su = room / kUnpackedStageBytes;
+            su = room / ub;
             if (su > kMaxUnpackedStages) su = kMaxUnpackedStages;
             sp = 0;
         } else {
@@ -214,23 +223,38 @@ struct Layout {
             if (sp > kMaxPackedStages) sp = kMaxPackedStages;
         }
         off_u = a_bytes;
-        off_p = off_u + (su > 0 ? su : 0) * kUnpackedStageBytes;
+        off_p = off_u + (su > 0 ? su : 0) * ub;
         off_bar = off_p + (sp > 0 ? sp : 0) * kPackedStageBytes;
-        total = off_bar + kBarBytes;
+        total = off_bar + kBarBytes + kPubBytes;
     }
     __host__ __device__ bool fits() const { return su >= 2 && (img || sp >= 2) && total <= kSmemLimit; }
 };
 
-template <int F, int MODE, int KP, bool SA, bool IMG>
-__global__ void __launch_bounds__(kThreads, 1)
+// PAIR: a CTA pair (cluster of 2) issues cta_group::2 MMAs with M = 256 (each
+// CTA's 128 unknowns) and N = BN knowns, each CTA streaming only its half of
+// the known tile (BN/2 rows of the prepared image) -- half the L2->SM operand
+// traffic per MAC of the single-CTA kernel, which is L2-throughput-bound.
+// The leader (rank 0) issues every MMA; the commits multicast to both CTAs.
+template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
+__global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     tensor_kernel(const __grid_constant__ CUtensorMap tmap, CompareArgs a, const uint8_t* __restrict__ a_global,
                   int64_t n_tiles, int n_slices) {
+    static_assert(!PAIR || (F == FASTID_TENSOR_F4 && IMG && !SA), "pairs run the prepared mxf4 image only");
     constexpr int BN = Fmt<F>::BN;
     constexpr int CPW = Fmt<F>::kCoresPerWord;
+    // the mxf4 image is stored in the pair layout: each stage = two BN/2-row halves
+    constexpr bool kSplitB = IMG && F == FASTID_TENSOR_F4;
     constexpr int UB = Layout<F>::kUnpackedStageBytes;
+    constexpr int HB = UB / 2;                 // one half of an image stage
+    constexpr int RB = PAIR ? HB : UB;         // bytes this CTA receives per stage
     constexpr int PB = Layout<F>::kPackedStageBytes;
+    using R = Roles<F, IMG>;
+    constexpr int kConvWarps = R::kConvWarps, kConvThreads = 32 * R::kConvWarps;
+    constexpr int kEpiWarps = R::kEpiWarps, kEpiThreads = 32 * R::kEpiWarps;
+    constexpr int kBuildWarps = R::kBuildWarps;
+    constexpr int kFirstEpiWarp = R::kFirstEpiWarp, kProducerWarp = R::kProducerWarp, kMmaWarp = R::kMmaWarp;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const Layout<F> lay(a.stride, SA, IMG);
+    const Layout<F> lay(a.stride, SA, IMG, PAIR);
     constexpr int AB = Layout<F>::kAStageBytes;
     const int SP = lay.sp;
     const int SU = lay.su;
@@ -249,12 +273,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* ar_full = a_full + 1;  // streamed-A ring
     uint64_t* ar_empty = ar_full + kMaxAStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ar_empty + kMaxAStages);
+    // published top-k admission bounds [split][unknown]; only ever decrease, so a
+    // stale read is a looser (still correct) bound
+    volatile uint32_t* pub = reinterpret_cast<volatile uint32_t*>(smem + lay.off_bar + Layout<F>::kBarBytes);
+    for (int i = threadIdx.x; i < kMaxSplits * kM; i += blockDim.x) pub[i] = 0xFFFFFFFFu;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int group = blockIdx.x / n_slices;
-    const int slice = blockIdx.x - group * n_slices;
-    const int64_t q0 = (int64_t)group * kM;
+    const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // CTA pair or CTA
+    const int group = unit / n_slices;
+    const int slice = unit - group * n_slices;
+    const int64_t q0 = ((int64_t)group * (PAIR ? 2 : 1) + rank) * kM;
     const int64_t t_begin = n_tiles * slice / n_slices;
     const int64_t t_end = n_tiles * (slice + 1) / n_slices;
 
@@ -269,9 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&t_full[i], 1);
-            ptx::mbar_init(&t_empty[i], IMG ? kEpiThreads + kConvThreads : kEpiThreads);
+            // pairs: one arrival per epilogue warp of both CTAs (on the leader's barrier)
+            ptx::mbar_init(&t_empty[i], PAIR ? 2 * kEpiWarps : kEpiThreads);
         }
-        ptx::mbar_init(a_full, kConvThreads);
+        ptx::mbar_init(a_full, PAIR ? 2 * kBuildWarps : 32 * kBuildWarps);
         for (int i = 0; i < kMaxAStages; ++i) {
             ptx::mbar_init(&ar_full[i], 1);
             ptx::mbar_init(&ar_empty[i], 1);
@@ -279,7 +311,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::fence_mbar_init();
     }
     if (warp == kProducerWarp && lane == 0) ptx::prefetch_tmap(&tmap);
-    if (warp == kMmaWarp) ptx::tmem_alloc(tmem_slot, Fmt<F>::kTmemCols);
+    if (PAIR) ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA
+    if (warp == kMmaWarp) {
+        if (PAIR)
+            ptx::tmem_alloc_pair(tmem_slot, Fmt<F>::kTmemCols);
+        else
+            ptx::tmem_alloc(tmem_slot, Fmt<F>::kTmemCols);
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -296,8 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
 
     if (warp == kProducerWarp) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
+        // ---------------- TMA producer (whole warp; one elected lane issues) ----------------
+        {
             Ring ra(SA ? lay.sa : 1), rp(SP > 0 ? SP : 1), ru(SU);
             for (int64_t t = t_begin; t < t_end; ++t) {
                 for (int ks = 0; ks < n_kst; ++ks, rp.next()) {
@@ -305,41 +343,80 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // this stage's slice of the pre-unpacked A operand (one bulk copy)
                         const int sa = ra.idx;
                         ptx::mbar_wait(&ar_empty[sa], ra.phase ^ 1);
-                        ptx::mbar_expect_tx(&ar_full[sa], AB);
-                        ptx::bulk_load(sA + sa * AB, a_global + ((int64_t)group * n_kst + ks) * AB, AB, &ar_full[sa]);
+                        if (ptx::elect_one()) {
+                            ptx::mbar_expect_tx(&ar_full[sa], AB);
+                            ptx::bulk_load(sA + sa * AB, a_global + ((int64_t)group * n_kst + ks) * AB, AB,
+                                           &ar_full[sa]);
+                        }
+                        __syncwarp();
                         ra.next();
+                    }
+                    if (PAIR) {
+                        // this CTA's half of the stage (tensor map over the image, box = one
+                        // half); completion is counted on the leader's barrier, which expects both
+                        ptx::mbar_wait(&u_empty[ru.idx], ru.phase ^ 1);
+                        if (ptx::elect_one()) {
+                            if (a.debug_flags & 4) {  // timing experiment: no operand traffic
+                                if (leader) ptx::mbar_arrive(&u_full[ru.idx]);
+                            } else {
+                                if (leader) ptx::mbar_expect_tx(&u_full[ru.idx], 2 * HB);
+                                ptx::tma_load_2d_pair(sU + ru.idx * HB, &tmap, ptx::mapa(&u_full[ru.idx], 0), 0,
+                                                      (int)(((t * n_kst + ks) * 2 + rank) * (BN / 2)));
+                            }
+                        }
+                        __syncwarp();
+                        ru.next();
+                        continue;
                     }
                     if (IMG) {
                         // the known tile's stage, already unpacked: one bulk copy into the operand ring
                         ptx::mbar_wait(&u_empty[ru.idx], ru.phase ^ 1);
-                        ptx::mbar_expect_tx(&u_full[ru.idx], UB);
-                        ptx::bulk_load(sU + ru.idx * UB, a.image + (t * n_kst + ks) * (int64_t)UB, UB,
-                                       &u_full[ru.idx]);
+                        if (ptx::elect_one()) {
+                            ptx::mbar_expect_tx(&u_full[ru.idx], UB);
+                            ptx::bulk_load(sU + ru.idx * UB, a.image + (t * n_kst + ks) * (int64_t)UB, UB,
+                                           &u_full[ru.idx]);
+                        }
+                        __syncwarp();
                         ru.next();
                         continue;
                     }
                     const int s = rp.idx;
                     ptx::mbar_wait(&p_empty[s], rp.phase ^ 1);
-                    ptx::mbar_expect_tx(&p_full[s], PB);
-                    ptx::tma_load_2d(sP + s * PB, &tmap, &p_full[s], ks * kStageBytesPacked, (int)(t * BN));
+                    if (ptx::elect_one()) {
+                        ptx::mbar_expect_tx(&p_full[s], PB);
+                        ptx::tma_load_2d(sP + s * PB, &tmap, &p_full[s], ks * kStageBytesPacked, (int)(t * BN));
+                    }
+                    __syncwarp();
                 }
             }
         }
     } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer (one thread) ----------------
-        if (lane == 0) {
-            constexpr uint32_t idesc = F == FASTID_TENSOR_F4 ? ptx::idesc_mxf4(kM, BN) : ptx::idesc_i8(kM, BN);
+        // ---------------- MMA issuer (the leader's warp for a pair; one elected lane issues) ----------------
+        if (leader) {
+            constexpr uint32_t idesc = PAIR ? ptx::idesc_mxf4(2 * kM, BN)
+                                            : (kSplitB ? ptx::idesc_mxf4(kM, BN / 2)
+                                                       : (F == FASTID_TENSOR_F4 ? ptx::idesc_mxf4(kM, BN)
+                                                                                : ptx::idesc_i8(kM, BN)));
+            constexpr int kBRows = kSplitB ? BN / 2 : BN;  // rows per B core-matrix column
             const uint64_t a_desc0 = ptx::smem_desc(ptx::smem_u32(sA), kM * 16, 128);
-            const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(sU), BN * 16, 128);
-            if (!SA) ptx::mbar_wait(a_full, 0);
+            const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(sU), kBRows * 16, 128);
+            if (!SA) {
+                if (PAIR)
+                    ptx::mbar_wait_cluster(a_full, 0);
+                else
+                    ptx::mbar_wait(a_full, 0);
+            }
             ptx::tc_fence_after();
             Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
             for (int64_t t = t_begin; t < t_end; ++t, ++local) {
                 const int acc = local & 1;
-                const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles;
+                const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
                 if (tr) a.trace[local * kTrSlots + kTrMmaWait] = clock64();
-                ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
+                if (PAIR)
+                    ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
+                else
+                    ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
                 if (tr) a.trace[local * kTrSlots + kTrMmaGo] = clock64();
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
@@ -347,32 +424,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = ru.idx;
                     const int sa = ra.idx;
                     if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
+                    const bool trs = tr && (a.debug_flags & 8) && ks < 16;
+                    if (trs) a.trace[local * kTrSlots + kTrB0Loaded + ks] = clock64();
                     ptx::mbar_wait(&u_full[s], ru.phase);
+                    if (trs) a.trace[local * kTrSlots + kTrB0Done + ks] = clock64();
                     ptx::tc_fence_after();
                     // descriptors of this stage's first K-step; later steps add fixed strides
                     const uint32_t a_off = SA ? (uint32_t)(sa * AB) : (uint32_t)(ks * kWordsPerStage * CPW) * (kM * 16);
                     const uint64_t ad = a_desc0 + (uint64_t)(a_off >> 4);
-                    const uint64_t bd = b_desc0 + (uint64_t)(((uint32_t)s * UB) >> 4);
-                    const uint64_t a_step = (2 * kM * 16) >> 4, b_step = (2 * BN * 16) >> 4;
-                    if (F == FASTID_TENSOR_F4)
-                        ptx::mma_mxf4_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol, tmem + kSfbCol,
-                                             ks ? 1u : 0u);
-                    else
-                        ptx::mma_i8_stage8(d, ad, bd, a_step, b_step, idesc, ks ? 1u : 0u);
-                    ptx::tc_commit(&u_empty[s]);  // stage s reusable once these MMAs retire
-                    if (SA) {
-                        ptx::tc_commit(&ar_empty[sa]);
-                        ra.next();
+                    const uint64_t bd = b_desc0 + (uint64_t)(((uint32_t)s * RB) >> 4);
+                    const uint64_t a_step = (2 * kM * 16) >> 4, b_step = (2 * kBRows * 16) >> 4;
+                    if (ptx::elect_one()) {
+                        if (PAIR) {
+                            ptx::mma_mxf4_pair_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol,
+                                                      tmem + kSfbCol, ks ? 1u : 0u);
+                            ptx::tc_commit_pair(&u_empty[s], 0x3);  // both halves of stage s reusable
+                        } else {
+                            if (kSplitB)
+                                ptx::mma_mxf4_split_stage4(d, BN / 2, ad, bd, (uint64_t)(HB >> 4), a_step, b_step,
+                                                           idesc, tmem + kSfaCol, tmem + kSfbCol, ks ? 1u : 0u);
+                            else if (F == FASTID_TENSOR_F4)
+                                ptx::mma_mxf4_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol, tmem + kSfbCol,
+                                                     ks ? 1u : 0u);
+                            else
+                                ptx::mma_i8_stage8(d, ad, bd, a_step, b_step, idesc, ks ? 1u : 0u);
+                            ptx::tc_commit(&u_empty[s]);  // stage s reusable once these MMAs retire
+                            if (SA) ptx::tc_commit(&ar_empty[sa]);
+                        }
                     }
+                    __syncwarp();
+                    if (SA) ra.next();
                 }
-                ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
+                if (ptx::elect_one()) {
+                    if (PAIR)
+                        ptx::tc_commit_pair(&t_full[acc], 0x3);  // both CTAs' accumulators complete
+                    else
+                        ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
+                }
+                __syncwarp();
                 if (tr) a.trace[local * kTrSlots + kTrMmaIssued] = clock64();
             }
         }
-    } else if (warp < kFirstEpiWarp) {
-        // ---------------- converters ----------------
-        const int ct = threadIdx.x;  // 0..kConvThreads-1
-        {
+    } else {
+        const int ct = threadIdx.x;  // 0..kConvThreads-1 for converters
+        if (warp < kBuildWarps) {
             // Resident A = complemented unknown rows; zero past the row.  Threads
             // 0..127 each build one row.
             if (!SA && ct < kM) {
@@ -402,13 +497,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::fence_proxy_async_smem();
-            ptx::mbar_arrive(a_full);
+            if (PAIR) {
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(a_full, 0));
+            } else {
+                ptx::mbar_arrive(a_full);
+            }
         }
-        if (IMG) goto epilogue;
-        {
+        if (warp < kFirstEpiWarp) {
+        // ---------------- converters ----------------
         // Work unit = (known row, 16-byte half of the stage): 2*BN units per stage.
         constexpr int kUnits = 2 * BN;
-        constexpr int kUnitsPerThread = (kUnits + kConvThreads - 1) / kConvThreads;
+        constexpr int kUnitsPerThread = kConvThreads ? (kUnits + kConvThreads - 1) / (kConvThreads ? kConvThreads : 1) : 1;
         Ring rp(SP), ru(SU);
         for (int64_t t = t_begin; t < t_end; ++t) {
             for (int ks = 0; ks < n_kst; ++ks, rp.next(), ru.next()) {
@@ -451,22 +551,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_arrive(&u_full[su]);
             }
         }
-        }
-    }
-    if (warp < kProducerWarp && (warp >= kFirstEpiWarp || IMG)) {
-    epilogue:;
+        } else {
         // ---------------- epilogue: one unknown per thread ----------------
         // A warp reads TMEM lanes 32*(w%4).. (its quadrant) and 1/n_splits of the
         // accumulator columns, in batches of up to 32 columns (x8 loads, one
         // wait per batch).  Scores stay raw accumulator bits (fp32 of an exact
         // integer orders like u32), so the hot path is a 3-input-min tree and
         // one compare per batch; candidates take a rare per-lane slow path.
-        constexpr int kSplitsMain = kEpiWarps / 4;                       // 2
-        constexpr int kSplits = IMG ? (kEpiWarps + kConvWarps) / 4 : kSplitsMain;  // 4 with an image
-        static_assert(kSplits <= kMaxSplits, "split count");
-        constexpr int kCols = BN / kSplits;  // 112 / 56 (mxf4), 64 / 32 (i8)
-        static_assert(kCols % 8 == 0, "columns per split must be a multiple of 8");
-        const int ew = IMG ? warp : warp - kFirstEpiWarp;
+        constexpr int kSplits = kEpiWarps / 4;  // 2 (packed) / 3 (mxf4 image) / 4 (i8 image)
+        static_assert(kSplits <= kMaxSplits && kSplits * 4 == kEpiWarps, "split count");
+        constexpr int kCols = BN / kSplits;  // 96 / 64 (mxf4), 64 / 32 (i8)
+        static_assert(kCols * kSplits == BN && kCols % 8 == 0, "columns per split must be a multiple of 8");
+        // with an image every column of a split is loaded before any compare work
+        constexpr bool kPreload = IMG && kCols <= 2 * kBatch;
+        constexpr int kPreBatches = (kCols + kBatch - 1) / kBatch;
+        const int ew = warp - kFirstEpiWarp;
         const int quad = warp & 3;
         const int split = ew >> 2;
         const int m = quad * 32 + lane;
@@ -476,29 +575,152 @@ __global__ void __launch_bounds__(kThreads, 1)
         TopList<KP> top;
         if (MODE == kTopK) top.clear();
         const uint64_t cap = (uint64_t)a.max_score + 1;  // admit v <= max_score
-        uint32_t thr_bits = 0;
+        uint32_t thr_bits = 0;  // own list: admit v < thr_bits (rows arrive in index order)
         if (MODE == kTopK) thr_bits = score_bits<F>(cap < kEmptyScore ? (uint32_t)cap : kEmptyScore);
+        // Admission bound shared by the splits of one unknown: a value worse than
+        // another split's k-th best cannot be in the union's top k (that split
+        // holds k values <= it, ties resolved by the merge), so each split admits
+        // v <= min over splits of their k-th best -- stored as bits + 1.
+        uint32_t thr_eff = thr_bits;
         const uint32_t hit_bits = MODE == kThreshold ? score_bits<F>(a.threshold) : 0u;
+        uint32_t t_empty_leader[2] = {0u, 0u};
+        if (PAIR) {
+            t_empty_leader[0] = ptx::mapa(&t_empty[0], 0);
+            t_empty_leader[1] = ptx::mapa(&t_empty[1], 0);
+        }
         int local = 0;
         for (int64_t t = t_begin; t < t_end; ++t, ++local) {
             const int acc = local & 1;
             ptx::mbar_wait(&t_full[acc], (local >> 1) & 1);
             const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
             if (tr) a.trace[local * kTrSlots + kTrEpi0 + ew] = clock64();
+            if (MODE == kTopK && kSplits > 1) {
+#pragma unroll
+                for (int s2 = 0; s2 < kSplits; ++s2) {
+                    const uint32_t b = pub[s2 * kM + m];
+                    if (b < thr_eff) thr_eff = b;
+                }
+            }
             ptx::tc_fence_after();
             const int64_t r0 = t * BN + split * kCols;
             const int64_t rows_left = a.n_refs - r0;
             const int rl = !q_ok ? 0 : (rows_left >= kCols ? kCols : (rows_left > 0 ? (int)rows_left : 0));
             const bool full = rl == kCols;
             const uint32_t col_base = (uint32_t)(acc * BN + split * kCols);
+            // per-batch processing of up to 32 columns already in registers
+            auto process = [&](uint32_t(&v)[kBatch], int b0, int nb) {
+                const int left = rl - b0;
+                const uint32_t valid = full || left >= kBatch ? (nb == 32 ? 0xFFFFFFFFu : (1u << nb) - 1u)
+                                                              : (left <= 0 ? 0u : (1u << left) - 1u);
+                const int64_t rc = r0 + b0;
+                if (MODE == kFull) {
+#pragma unroll
+                    for (int c = 0; c < kBatch; ++c)
+                        if ((valid >> c) & 1u) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
+                    return;
+                }
+                if (valid != 0xFFFFFFFFu) {
+#pragma unroll
+                    for (int c = 0; c < kBatch; ++c)
+                        if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
+                }
+                const uint32_t mn = min32(v);
+                if (MODE == kTopK) {
+                    if (mn < thr_eff) {
+                        uint32_t cand = 0;
+#pragma unroll
+                        for (int c = 0; c < kBatch; ++c) cand |= (v[c] < thr_eff ? 1u : 0u) << c;
+                        // rare: one insertion per loop trip, value picked by a select tree
+                        while (cand) {
+                            const int c = __ffs(cand) - 1;
+                            cand &= cand - 1;
+                            const uint32_t vc = pick32(v, c);
+                            if (vc < thr_eff) {
+                                top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
+                                const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
+                                thr_bits = score_bits<F>(w < kEmptyScore ? (uint32_t)w : kEmptyScore);
+                                if (thr_bits < thr_eff) thr_eff = thr_bits;
+                                if (kSplits > 1) pub[split * kM + m] = thr_bits == 0xFFFFFFFFu ? thr_bits : thr_bits + 1;
+                            }
+                        }
+                    }
+                } else {
+                    uint32_t hit = 0;
+                    if (mn <= hit_bits) {
+#pragma unroll
+                        for (int c = 0; c < kBatch; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
+                    }
+                    if (__any_sync(0xffffffffu, hit != 0)) {
+                        uint32_t all = __reduce_or_sync(0xffffffffu, hit);
+                        while (all) {  // warp-uniform walk over columns with a hit in any lane
+                            const int c = __ffs(all) - 1;
+                            all &= all - 1;
+                            emit_hits(a, (hit >> c) & 1u, (uint32_t)q, rc + c, decode_exact<F>(pick32(v, c)));
+                        }
+                    }
+                }
+            };
+            auto release = [&]() {
+                // this warp's columns are all in registers: release the accumulator
+                ptx::tc_fence_before();
+                if (PAIR) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(t_empty_leader[acc]);
+                } else {
+                    ptx::mbar_arrive(&t_empty[acc]);
+                }
+                if (tr) a.trace[local * kTrSlots + kTrRel0 + ew] = clock64();
+            };
+            const uint32_t ta0 = lane_base + col_base;
+            if (kPreload) {
+                // every column of this warp's split in one round of loads, one wait,
+                // the accumulator released at once, then the compare work
+                uint32_t v[kPreBatches][kBatch];
+                if (!(a.debug_flags & 1)) {
+#pragma unroll
+                    for (int b = 0; b < kPreBatches; ++b) {
+                        const int nb = kCols - b * kBatch < kBatch ? kCols - b * kBatch : kBatch;
+                        const uint32_t ta = ta0 + (uint32_t)(b * kBatch);
+                        if (nb == 32) {
+                            ptx::tmem_ld32(ta, v[b]);
+                        } else {
+                            int o = 0;
+                            if (nb - o >= 16) {
+                                ptx::tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(&v[b][0]));
+                                o = 16;
+                            }
+                            if (nb - o >= 8) {
+                                ptx::tmem_ld8(ta + (uint32_t)o, &v[b][o]);
+                                o += 8;
+                            }
+                            if (nb - o >= 8) ptx::tmem_ld8(ta + (uint32_t)o, &v[b][o]);
+                        }
+                    }
+                    ptx::tmem_wait_ld();
+                } else {
+#pragma unroll
+                    for (int b = 0; b < kPreBatches; ++b)
+#pragma unroll
+                        for (int c = 0; c < kBatch; ++c) v[b][c] = 0xFFFFFFFFu;
+                }
+                if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
+                release();
+#pragma unroll
+                for (int b = 0; b < kPreBatches; ++b) {
+                    const int nb = kCols - b * kBatch < kBatch ? kCols - b * kBatch : kBatch;
+                    process(v[b], b * kBatch, nb);
+                }
+                if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
+                continue;
+            }
 #pragma unroll
             for (int b0 = 0; b0 < kCols; b0 += kBatch) {
-                if (tr && b0 == kBatch) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
+                if (tr && b0 == kBatch && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
                 const int nb = kCols - b0 < kBatch ? kCols - b0 : kBatch;  // multiple of 8, warp-uniform
                 uint32_t v[kBatch];
                 if (!(a.debug_flags & 1)) {
                     // widest loads that fit (x32 moves ~40% more TMEM bytes/clk than x8)
-                    const uint32_t ta = lane_base + col_base + (uint32_t)b0;
+                    const uint32_t ta = ta0 + (uint32_t)b0;
                     if (nb == 32) {
                         ptx::tmem_ld32(ta, v);
                     } else {
@@ -518,61 +740,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < kBatch; ++c) v[c] = 0xFFFFFFFFu;
                 }
-                if (tr && b0 == 0) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
-                if (b0 + kBatch >= kCols) {
-                    // this warp's columns are all in registers: release the accumulator
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(&t_empty[acc]);
-                    if (tr) a.trace[local * kTrSlots + kTrRel0 + ew] = clock64();
-                }
-                const int left = rl - b0;
-                const uint32_t valid = full || left >= kBatch ? (nb == 32 ? 0xFFFFFFFFu : (1u << nb) - 1u)
-                                                              : (left <= 0 ? 0u : (1u << left) - 1u);
-                const int64_t rc = r0 + b0;
-                if (MODE == kFull) {
-#pragma unroll
-                    for (int c = 0; c < kBatch; ++c)
-                        if ((valid >> c) & 1u) a.out[(rc + c) * a.ld_out + q] = decode_fast<F>(v[c]);
-                    continue;
-                }
-                if (valid != 0xFFFFFFFFu) {
-#pragma unroll
-                    for (int c = 0; c < kBatch; ++c)
-                        if (!((valid >> c) & 1u)) v[c] = 0xFFFFFFFFu;
-                }
-                const uint32_t mn = min32(v);
-                if (MODE == kTopK) {
-                    if (mn < thr_bits) {
-                        uint32_t cand = 0;
-#pragma unroll
-                        for (int c = 0; c < kBatch; ++c) cand |= (v[c] < thr_bits ? 1u : 0u) << c;
-                        // rare: one insertion per loop trip, value picked by a select tree
-                        while (cand) {
-                            const int c = __ffs(cand) - 1;
-                            cand &= cand - 1;
-                            const uint32_t vc = pick32(v, c);
-                            if (vc < thr_bits) {
-                                top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
-                                const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
-                                thr_bits = score_bits<F>(w < kEmptyScore ? (uint32_t)w : kEmptyScore);
-                            }
-                        }
-                    }
-                } else {
-                    uint32_t hit = 0;
-                    if (mn <= hit_bits) {
-#pragma unroll
-                        for (int c = 0; c < kBatch; ++c) hit |= (v[c] <= hit_bits ? 1u : 0u) << c;
-                    }
-                    if (__any_sync(0xffffffffu, hit != 0)) {
-                        uint32_t all = __reduce_or_sync(0xffffffffu, hit);
-                        while (all) {  // warp-uniform walk over columns with a hit in any lane
-                            const int c = __ffs(all) - 1;
-                            all &= all - 1;
-                            emit_hits(a, (hit >> c) & 1u, (uint32_t)q, rc + c, decode_exact<F>(pick32(v, c)));
-                        }
-                    }
-                }
+                if (tr && b0 == 0 && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
+                if (b0 + kBatch >= kCols) release();
+                process(v, b0, nb);
             }
         }
         if (MODE == kTopK && q_ok) {
@@ -588,13 +758,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 empty.store(a.part_scores + off2, a.part_index + off2, a.ref_base);
             }
         }
+        }
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if (PAIR)
+        ptx::cluster_sync();  // the leader's MMAs and the peer's remote arrivals are all done
+    else
+        __syncthreads();
     if (warp == kMmaWarp) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, Fmt<F>::kTmemCols);
+        if (PAIR)
+            ptx::tmem_dealloc_pair(tmem, Fmt<F>::kTmemCols);
+        else
+            ptx::tmem_dealloc(tmem, Fmt<F>::kTmemCols);
     }
 }
 
@@ -683,13 +860,36 @@ __global__ void prep_a_kernel(CompareArgs a, int n_groups, int n_kst, uint8_t* _
 template <int F>
 bool use_stream_a(int64_t stride) { return !Layout<F>(stride, false).fits(); }
 
-template <int F, int MODE, int KP, bool SA, bool IMG>
+// Tensor map over the mxf4 image viewed as rows of 128 B: one box = one half
+// stage (BN/2 known rows x 256 loci in the UMMA layout, contiguous).
+template <int F>
+int make_image_map(CUtensorMap* map, const CompareArgs& a) {
+    auto fn = encode_fn();
+    if (!fn) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const Layout<F> lay(a.stride, false, true);
+    const int64_t bytes = ceil_div(a.n_refs, Fmt<F>::BN) * lay.n_kst * Layout<F>::kUnpackedStageBytes;
+    cuuint64_t dims[2] = {128, (cuuint64_t)(bytes / 128)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {128, (cuuint32_t)(Layout<F>::kUnpackedStageBytes / 2 / 128)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a.image, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled (image) failed (%d)", (int)r);
+    return FASTID_OK;
+}
+
+template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
 int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     CUtensorMap map;
-    if (int rc = make_known_map(&map, a, Fmt<F>::BN)) return rc;
-    const Layout<F> lay(a.stride, SA, IMG);
+    if (PAIR) {
+        if (int rc = make_image_map<F>(&map, a)) return rc;
+    } else {
+        if (int rc = make_known_map(&map, a, Fmt<F>::BN)) return rc;
+    }
+    const Layout<F> lay(a.stride, SA, IMG, PAIR);
     if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
-    auto kern = tensor_kernel<F, MODE, KP, SA, IMG>;
+    auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR>;
     FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     const int64_t groups = ceil_div(a.n_queries, kM);
     const int64_t tiles = ceil_div(a.n_refs, Fmt<F>::BN);
@@ -702,10 +902,45 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
             a, (int)groups, lay.n_kst, a_global);
         FASTID_LAUNCHED("prep_a_kernel");
     }
-    kern<<<(unsigned)(groups * n_slices), kThreads, lay.total, stream>>>(map, a, a_global, tiles, n_slices);
+    if (PAIR) {
+        const int64_t pairs = ceil_div(a.n_queries, 2 * kM) * n_slices;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(2 * pairs));
+        cfg.blockDim = dim3(Roles<F, IMG>::kThreads);
+        cfg.dynamicSmemBytes = (size_t)lay.total;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a, (const uint8_t*)a_global, tiles, n_slices));
+    } else {
+        kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, a, a_global, tiles,
+                                                                                         n_slices);
+    }
     FASTID_LAUNCHED("tensor_kernel");
     if (SA) FASTID_CUDA(cudaFreeAsync(a_global, stream));
     return FASTID_OK;
+}
+
+// CTA pairs run the prepared mxf4 image with a resident unknown tile.
+template <int F>
+bool use_pair(const CompareArgs& a) {
+    return F == FASTID_TENSOR_F4 && a.image != nullptr && !(a.debug_flags & 2) &&
+           Layout<F>(a.stride, false, true, true).fits();
+}
+
+template <int F>
+int pair_slices_for(int64_t n_refs, int64_t n_queries) {
+    const int64_t pgroups = ceil_div(n_queries, 2 * kM);
+    const int64_t tiles = ceil_div(n_refs, Fmt<F>::BN);
+    int64_t s = (num_sms() / 2) / (pgroups > 0 ? pgroups : 1);
+    if (s > tiles) s = tiles;
+    if (s < 1) s = 1;
+    return (int)s;
 }
 
 template <int F, int MODE, int KP>
@@ -713,11 +948,14 @@ int launch_one(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     const bool img = a.image != nullptr;
     const bool sa = !Layout<F>(a.stride, false, img).fits();
     if (img) {
-        if (sa) return launch_one_impl<F, MODE, KP, true, true>(a, n_slices, stream);
-        return launch_one_impl<F, MODE, KP, false, true>(a, n_slices, stream);
+        if constexpr (F == FASTID_TENSOR_F4) {
+            if (use_pair<F>(a)) return launch_one_impl<F, MODE, KP, false, true, true>(a, n_slices, stream);
+        }
+        if (sa) return launch_one_impl<F, MODE, KP, true, true, false>(a, n_slices, stream);
+        return launch_one_impl<F, MODE, KP, false, true, false>(a, n_slices, stream);
     }
-    if (sa) return launch_one_impl<F, MODE, KP, true, false>(a, n_slices, stream);
-    return launch_one_impl<F, MODE, KP, false, false>(a, n_slices, stream);
+    if (sa) return launch_one_impl<F, MODE, KP, true, false, false>(a, n_slices, stream);
+    return launch_one_impl<F, MODE, KP, false, false, false>(a, n_slices, stream);
 }
 
 // Tensor image of a known panel: for every (tile, stage) the UMMA-layout B
@@ -743,10 +981,14 @@ __global__ void build_image_kernel(CompareArgs a, int64_t n_tiles, int n_kst, ui
         uint8_t* dst = image + blk * UB;
         const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
         const int col0 = half * 4 * CPW;
+        // mxf4: pair layout -- rows [0, BN/2) then [BN/2, BN), each its own
+        // K-major block of BN/2 rows (the half a CTA of a pair streams)
+        const int hr = row >= BN / 2 ? 1 : 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if (F == FASTID_TENSOR_F4) {
-                *reinterpret_cast<uint4*>(dst + core_off(row, col0 + i, BN)) = unpack_f4<true>(wv[i]);
+                *reinterpret_cast<uint4*>(dst + hr * (UB / 2) + core_off(row - hr * (BN / 2), col0 + i, BN / 2)) =
+                    unpack_f4<true>(wv[i]);
             } else {
                 uint4 lo, hi;
                 unpack_i8<true>(wv[i], lo, hi);
@@ -777,7 +1019,7 @@ int build_image_fmt(const CompareArgs& a, void* image, cudaStream_t stream) {
 
 template <int F>
 int launch_fmt(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t stream) {
-    const int slices = slices_for<F>(a.n_refs, a.n_queries);
+    const int slices = use_pair<F>(a) ? pair_slices_for<F>(a.n_refs, a.n_queries) : slices_for<F>(a.n_refs, a.n_queries);
     if (mode == kFull) return launch_one<F, kFull, 1>(a, slices, stream);
     if (mode == kThreshold) return launch_one<F, kThreshold, 1>(a, slices, stream);
     *n_parts = kMaxSplits * slices;  // one partial list per (slice, epilogue column split)
@@ -814,8 +1056,10 @@ int build_tensor_image(const CompareArgs& a, int formulation, void* image, cudaS
 }
 
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation) {
+    // an upper bound: the launch reports the partition it used
     if (formulation == FASTID_TENSOR_I8) return kMaxSplits * slices_for<FASTID_TENSOR_I8>(n_refs, n_queries);
-    return kMaxSplits * slices_for<FASTID_TENSOR_F4>(n_refs, n_queries);
+    return kMaxSplits * std::max(slices_for<FASTID_TENSOR_F4>(n_refs, n_queries),
+                                 pair_slices_for<FASTID_TENSOR_F4>(n_refs, n_queries));
 }
 
 int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream) {

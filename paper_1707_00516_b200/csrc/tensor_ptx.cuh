@@ -60,6 +60,69 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+// One lane of the (converged) warp returns true.  Issue paths keep the whole
+// warp in the loop and elect the issuing lane only around the instruction, so
+// loop state and descriptors stay warp-uniform (uniform registers, no per-MMA
+// R2UR waterfall).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n"
+        ".reg .b32 rx;\n"
+        ".reg .pred px;\n"
+        "elect.sync rx|px, %1;\n"
+        "@px mov.s32 %0, 1;\n"
+        "}\n"
+        : "+r"(pred)
+        : "r"(0xFFFFFFFFu));
+    return pred != 0;
+}
+
+// ---- clusters (CTA pairs for cta_group::2) ----------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// Arrive on an mbarrier given by its shared::cluster address (default .release.cta
+// semantics, as CUTLASS's ClusterBarrier::arrive: the arrivals here only order
+// completed tcgen05.ld / async-proxy work, and a cluster-scope release would
+// fence every prior global store of the thread).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+// Wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 2-D tensor copy into this CTA's shared memory whose completion is counted on
+// an mbarrier of either CTA of the pair (shared::cluster address).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x,
+                                                 int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+
 // ---- tcgen05 ---------------------------------------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
@@ -70,6 +133,16 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// CTA-pair TMEM allocation: issued by the same warp of both CTAs.
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -77,6 +150,16 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                  : "memory");
+}
+
+// Pair commit: arrive on the mbarrier at the same offset in every CTA of `mask`
+// once the pair MMAs issued so far by this thread complete.
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 
 // D[tmem] (+)= A[smem] . B[smem]^T, int8 operands, int32 accumulate.
@@ -130,6 +213,45 @@ __device__ __forceinline__ void mma_mxf4_stage4(uint32_t tmem_d, uint64_t ad, ui
         "}\n" ::"r"(tmem_d),
         "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb), "l"(a_step), "l"(b_step)
         : "memory");
+}
+// The same stage as a CTA pair (cta_group::2, M = 256): A rows 0-127 come from
+// the leader's shared memory and 128-255 from the peer's, B rows 0..N/2-1 from
+// the leader's and N/2..N-1 from the peer's, at identical offsets; each CTA's
+// TMEM receives its own 128 rows of D.
+__device__ __forceinline__ void mma_mxf4_pair_stage4(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint64_t a_step,
+                                                     uint64_t b_step, uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                                     uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, t;\n"
+        ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.u32 t, 0, 0;\n"
+        "add.s64 a1, %1, %7; add.s64 b1, %2, %8;\n"
+        "add.s64 a2, a1, %7; add.s64 b2, b1, %8;\n"
+        "add.s64 a3, a2, %7; add.s64 b3, b2, %8;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a1, b1, %3, [%5], [%6], t;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a2, b2, %3, [%5], [%6], t;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a3, b3, %3, [%5], [%6], t;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb), "l"(a_step), "l"(b_step)
+        : "memory");
+}
+// One stage on a single CTA whose B operand is split in two row halves (the
+// pair layout of the prepared image): two N/2 MMAs per K-step into adjacent
+// accumulator column ranges.
+__device__ __forceinline__ void mma_mxf4_split_stage4(uint32_t tmem_d, uint32_t half_cols, uint64_t ad, uint64_t bd,
+                                                      uint64_t b_half, uint64_t a_step, uint64_t b_step,
+                                                      uint32_t idesc_half, uint32_t sfa, uint32_t sfb,
+                                                      uint32_t accumulate) {
+    const uint32_t d1 = tmem_d + half_cols;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t acc = j ? 1u : accumulate;
+        mma_mxf4(tmem_d, ad + j * a_step, bd + j * b_step, idesc_half, sfa, sfb, acc);
+        mma_mxf4(d1, ad + j * a_step, bd + b_half + j * b_step, idesc_half, sfa, sfb, acc);
+    }
 }
 __device__ __forceinline__ void mma_i8_stage8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint64_t a_step,
                                               uint64_t b_step, uint32_t idesc, uint32_t accumulate) {

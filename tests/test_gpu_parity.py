@@ -244,3 +244,41 @@ def test_prepared_database_image(rng, form, L):
     hits = db.threshold(m.Panel(tuple(range(150)), q, L), thr)
     hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
     assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 1000) and np.array_equal(hits.score, hs)
+
+
+@pytest.mark.parametrize("pairs", [True, False])
+@pytest.mark.parametrize("shape", [(1137, 129, 1024), (2500, 520, 2048), (700, 300, 1800), (224, 256, 64)])
+def test_image_pairs_and_split(rng, pairs, shape):
+    """Prepared mxf4 image: the CTA-pair kernel (cta_group::2, M=256) and the
+    single-CTA split-B kernel (debug flag 2) both equal the oracle, for every
+    epilogue, with ragged unknown groups and known tiles."""
+    m = fb()
+    from paper_1707_00516_b200 import _native
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    n_r, n_q, L = shape
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    q, _ = rand_words(rng, n_q, nw, 64, L)
+    q[: n_q // 4] = r[rng.integers(0, n_r, n_q // 4)]
+    r[n_r // 2 : n_r // 2 + 3] = r[:3]
+    lib = _native.lib()
+    lib.fastid_debug_flags(0 if pairs else 2)
+    try:
+        db = KnownDatabase(r, L, formulation="tensor_f4", ref_base=7)
+        dq = m.DevicePanel.from_words(q, L)
+        exp = oracle.naive(r, q)
+        full = db.full_device(dq).cpu().numpy().view(np.uint32)
+        assert np.array_equal(full, exp)
+        for k in (1, 16, 32):
+            s, x = db.search_words(q, k)
+            es, ex, _ = oracle.topk_from_matrix(exp, k)
+            assert np.array_equal(s, es), k
+            assert np.array_equal(x, np.where(ex >= 0, ex + 7, -1)), k
+        thr = int(np.percentile(exp, 2))
+        hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
+        hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
+        assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 7)
+        assert np.array_equal(hits.score, hs)
+    finally:
+        lib.fastid_debug_flags(0)

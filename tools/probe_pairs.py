@@ -1,0 +1,26 @@
+"""Tensor-pipe probe: single-CTA vs CTA-pair mxf4 MMA throughput (resident operands)."""
+import ctypes, sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+from paper_1707_00516_b200 import _native
+
+L = _native.lib()
+scratch = torch.zeros(4096, dtype=torch.int32, device="cuda")
+src = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
+names = {8 + 128 + 4 + 256: "pair N=192 tiled walk", 8 + 128 + 4 + 256 + 64: "pair N=192 tiled walk commit/4",
+         8 + 128 + 4 + 256 + 512: "pair N=192 tiled walk wait/4", 8 + 128 + 4 + 256 + 512 + 64: "pair N=192 tiled walk wait+commit/4",
+         8 + 4 + 256 + 512 + 64: "pair N=224 tiled walk wait+commit/4"}
+for variant, name in names.items():
+    best = 0
+    for rep in range(4):
+        work = ctypes.c_double(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _native.check(L.fastid_probe_variant(_native.formulation_code("tensor_f4"), variant, 40000,
+                                             scratch.data_ptr(), src.data_ptr(), src.numel(), ctypes.byref(work),
+                                             torch.cuda.current_stream().cuda_stream), "probe")
+        e1.record(); e1.synchronize()
+        if rep:
+            best = max(best, work.value / (e0.elapsed_time(e1) / 1e3))
+    print(f"{name:28s}: {2*best/1e12:8.1f} TFLOP/s-equiv", flush=True)
