@@ -83,6 +83,23 @@ struct TopList {
             x[p] = tx;
         }
     }
+    // Insert a value whose index is larger than every index already listed (a
+    // scan in row order), so it goes after every entry with score <= v.  All K
+    // positions update in parallel from one predicate vector: depth 3 instead
+    // of the K-step dependent chain of insert().
+    __device__ __forceinline__ void insert_last(uint32_t v, uint32_t idx) {
+        bool le[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) le[i] = s[i] <= v;
+#pragma unroll
+        for (int i = K - 1; i > 0; --i) {
+            const bool prev_le = le[i - 1];
+            s[i] = le[i] ? s[i] : (prev_le ? v : s[i - 1]);
+            x[i] = le[i] ? x[i] : (prev_le ? idx : x[i - 1]);
+        }
+        s[0] = le[0] ? s[0] : v;
+        x[0] = le[0] ? x[0] : idx;
+    }
     __device__ __forceinline__ void offer(uint32_t v, uint32_t idx, uint32_t max_score) {
         if (v <= max_score && admits(v, idx)) insert(v, idx);
     }
@@ -115,6 +132,7 @@ struct CompareArgs {
     uint32_t* part_scores;  // [n_parts][n_queries][kpad]
     int64_t* part_index;
     int kpad;
+    uint32_t* bound;        // [n_queries] shared top-k admission bound (formulation's raw score bits: admit v < bound), or null
     // threshold
     uint32_t threshold;
     int64_t ref_base;
@@ -126,7 +144,7 @@ struct CompareArgs {
     // diagnostics (fastid_debug_trace): CTA 0 timestamps, or null
     long long* trace;
     int trace_tiles;
-    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 1: no CTA pairs; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits (timing experiments only)
+    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 1: no CTA pairs; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits; bit 4: no top-k insertions; bit 5: count insertions per tile (timing experiments only)
 };
 
 // Per-tile trace slots written by CTA 0 when tracing is on (clock64 values).

@@ -150,35 +150,53 @@ __global__ void __launch_bounds__(128, 1) mma_pair_probe_kernel(int iters, uint3
     ptx::tc_fence_before();
     ptx::cluster_sync();
     ptx::tc_fence_after();
-    if (threadIdx.x == 0 && rank == 0) {
+    if (warp == 0 && rank == 0) {
+        // whole warp in the loop, one elected lane issues (as the comparison kernel)
         const uint32_t a = ptx::smem_u32(smem);
         const uint32_t b = a + 64 * 1024;
         const int chunks = walk ? 16 : 1;
-        for (int i = 0; i < iters; ++i) {
-            // walk & 32: a (satisfied) mbarrier wait + tcgen05 fence before every 4 MMAs
-            if ((walk & 32) && (i & 3) == 0) {
+        const bool tiled = (walk & 16) != 0;
+        const int group = (walk & 64) ? 8 : 4;  // MMAs per stage (wait / commit granularity)
+        const int bufs = (walk & 128) ? 3 : 2;
+        for (int i0 = 0; i0 < iters; i0 += 4) {
+            const bool stage_start = (i0 % group) == 0;
+            const bool stage_end = ((i0 + 4) % group) == 0;
+            // walk & 32: a (satisfied) mbarrier wait + tcgen05 fence before every stage
+            if ((walk & 32) && stage_start) {
                 ptx::mbar_wait(&open_bar, 0);
                 ptx::tc_fence_after();
             }
-            const int c = i % chunks;
-            const uint64_t ad = ptx::smem_desc(a + (uint32_t)(c * 4096), 128 * 16, 128);
-            const uint64_t bd = ptx::smem_desc(b + (uint32_t)(c * (BN / 2) * 32), (BN / 2) * 16, 128);
-            // walk & 16: the real kernel's tile structure -- 16 K-steps into one of two
-            // accumulators at column offset 0 / BN, the first step of a tile overwriting
-            const bool tiled = (walk & 16) != 0;
-            const uint32_t d = tmem + (uint32_t)(tiled ? ((i >> 4) & 1) * BN
-                                                       : ((walk & 2) ? 0 : (i & 1) * (BN <= 224 ? 224 : 256)));
-            const uint32_t accf = tiled ? (uint32_t)((i & 15) != 0) : (uint32_t)(i > 1);
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d),
-                "l"(ad), "l"(bd), "r"(ptx::idesc_mxf4(256, BN)), "r"(accf), "r"(tmem + 448),
-                "r"(tmem + 480)
-                : "memory");
-            // walk & 8: commit (multicast) after every 4 MMAs like the real kernel's stages
-            if ((walk & 8) && (i & 3) == 3) ptx::tc_commit_pair(&sink_bar[(i >> 2) & 7], 0x3);
+            // descriptors computed warp-uniformly, outside the elected region
+            uint64_t ad[4], bd[4];
+            uint32_t d[4], accf[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int i = i0 + j;
+                const int c = i % chunks;
+                ad[j] = ptx::smem_desc(a + (uint32_t)(c * 4096), 128 * 16, 128);
+                bd[j] = ptx::smem_desc(b + (uint32_t)(c * (BN / 2) * 32), (BN / 2) * 16, 128);
+                // walk & 16: the real kernel's tile structure -- 16 K-steps into one of
+                // `bufs` accumulators at column offset k*BN, the first step overwriting
+                d[j] = tmem + (uint32_t)(tiled ? ((i >> 4) % bufs) * BN
+                                               : ((walk & 2) ? 0 : (i & 1) * (BN <= 224 ? 224 : 256)));
+                accf[j] = tiled ? (uint32_t)((i & 15) != 0) : (uint32_t)(i > 1);
+            }
+            if (ptx::elect_one()) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d[j]),
+                        "l"(ad[j]), "l"(bd[j]), "r"(ptx::idesc_mxf4(256, BN)), "r"(accf[j]), "r"(tmem + 448),
+                        "r"(tmem + 480)
+                        : "memory");
+                // walk & 8: commit (multicast) after every stage like the real kernel
+                if ((walk & 8) && stage_end) ptx::tc_commit_pair(&sink_bar[(i0 / group) & 7], 0x3);
+            }
+            __syncwarp();
         }
-        ptx::tc_commit_pair(&done, 0x3);
+        if (ptx::elect_one()) ptx::tc_commit_pair(&done, 0x3);
+        __syncwarp();
     }
     if (threadIdx.x == 0) ptx::mbar_wait(&done, 0);
     ptx::tc_fence_before();
@@ -381,7 +399,10 @@ extern "C" int fastid_probe_variant(int formulation, int variant, int iters, voi
         // CTA pairs: variant bit 4 selects N = 256 (else 224), bit 2 walks operand addresses
         const bool n256 = (variant & 16) != 0;
         const bool n192 = (variant & 128) != 0;
-        auto kern = n192 ? mma_pair_probe_kernel<192> : (n256 ? mma_pair_probe_kernel<256> : mma_pair_probe_kernel<224>);
+        const bool n144 = (variant & 1024) != 0;
+        auto kern = n144 ? mma_pair_probe_kernel<144>
+                         : (n192 ? mma_pair_probe_kernel<192>
+                                 : (n256 ? mma_pair_probe_kernel<256> : mma_pair_probe_kernel<224>));
         FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(sms & ~1));
@@ -397,9 +418,10 @@ extern "C" int fastid_probe_variant(int formulation, int variant, int iters, voi
         cfg.numAttrs = 1;
         // variant bit 0: one accumulator (K-loop dependency chain), bit 2: walk operand addresses
         FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, iters, sink, ((variant & 4) ? 1 : 0) | ((variant & 1) ? 2 : 0) | ((variant & 32) ? 4 : 0) |
-                                                             ((variant & 64) ? 8 : 0) | ((variant & 256) ? 16 : 0) | ((variant & 512) ? 32 : 0)));
+                                                             ((variant & 64) ? 8 : 0) | ((variant & 256) ? 16 : 0) | ((variant & 512) ? 32 : 0) |
+                                                             ((variant & 2048) ? 64 : 0) | ((variant & 4096) ? 128 : 0)));
         FASTID_LAUNCHED("mma_pair_probe_kernel");
-        *work = (double)(sms / 2) * iters * 256.0 * (n192 ? 192 : (n256 ? 256 : 224)) * 64.0;
+        *work = (double)(sms / 2) * iters * 256.0 * (n144 ? 144 : (n192 ? 192 : (n256 ? 256 : 224))) * 64.0;
         return FASTID_OK;
     }
     const int bn = f4 ? 224 : 128;

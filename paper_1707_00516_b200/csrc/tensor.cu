@@ -12,7 +12,7 @@
 //   warp 0      TMA producer: 2-D tensor copies of packed known rows
 //               (BN rows x 32 B = 256 loci per stage) into a deep ring.
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma into a
-//               double-buffered TMEM accumulator (BN fp32/s32 columns each).
+//               triple-buffered TMEM accumulator (BN fp32/s32 columns each).
 //   warps 2-5   converters: unpack the packed bits into the UMMA K-major
 //               operand layout (e2m1 nibbles or int8 bytes); at start-up they
 //               also build the resident A operand = complemented unknown tile.
@@ -58,6 +58,10 @@ struct Roles {
     static constexpr int kMmaWarp = kProducerWarp + 1;
     static constexpr int kThreads = 32 * (kMmaWarp + 1);
 };
+// Accumulator buffers in TMEM: the MMA fills one while the epilogue drains
+// the others, so an epilogue warp that runs late on one tile (top-k
+// insertions) does not stall the tensor pipe.
+constexpr int kAccBufs = 2;
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
 constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
 constexpr int kSmemLimit = 227 * 1024;
@@ -68,7 +72,7 @@ template <>
 struct Fmt<FASTID_TENSOR_I8> {
     static constexpr int BN = 128;          // knowns per tile (MMA N)
     static constexpr int kCoresPerWord = 2; // 16-B core columns produced per packed u32
-    static constexpr int kTmemCols = 256;   // 2 x BN accumulator columns
+    static constexpr int kTmemCols = 512;   // kAccBufs x BN accumulator columns
 };
 template <>
 struct Fmt<FASTID_TENSOR_F4> {
@@ -181,9 +185,7 @@ struct Layout {
     static constexpr int kUnpackedStageBytes = BN * 16 * kWordsPerStage * Fmt<F>::kCoresPerWord;
     static constexpr int kPackedStageBytes = BN * kStageBytesPacked;
     static constexpr int kAStageBytes = kM * 16 * kWordsPerStage * Fmt<F>::kCoresPerWord;
-    static constexpr int kBarBytes = 8 * (2 * kMaxPackedStages + 2 * kMaxUnpackedStages + 2 * kMaxAStages + 5) + 16;
-    // top-k: each epilogue split's published admission bound per unknown (u32 raw score bits)
-    static constexpr int kPubBytes = kMaxSplits * kM * 4;
+    static constexpr int kBarBytes = 8 * (2 * kMaxPackedStages + 2 * kMaxUnpackedStages + 2 * kMaxAStages + 2 * kAccBufs + 1) + 16;
     int n_kst;    // stages per tile (K padded to 256 loci)
     int a_bytes;  // resident A tile, or the A ring when streaming
     int sa;       // A ring depth (streamed A only)
@@ -209,7 +211,7 @@ struct Layout {
         }
     }
     __host__ __device__ void place() {
-        const int room = kSmemLimit - a_bytes - kBarBytes - kPubBytes;
+        const int room = kSmemLimit - a_bytes - kBarBytes;
         if (img) {
             // the tensor image is already in the UMMA layout: only the operand ring
             su = room / ub;
@@ -225,7 +227,7 @@ struct Layout {
         off_u = a_bytes;
         off_p = off_u + (su > 0 ? su : 0) * ub;
         off_bar = off_p + (sp > 0 ? sp : 0) * kPackedStageBytes;
-        total = off_bar + kBarBytes + kPubBytes;
+        total = off_bar + kBarBytes;
     }
     __host__ __device__ bool fits() const { return su >= 2 && (img || sp >= 2) && total <= kSmemLimit; }
 };
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     tensor_kernel(const __grid_constant__ CUtensorMap tmap, CompareArgs a, const uint8_t* __restrict__ a_global,
                   int64_t n_tiles, int n_slices) {
     static_assert(!PAIR || (F == FASTID_TENSOR_F4 && IMG && !SA), "pairs run the prepared mxf4 image only");
+    static_assert(kAccBufs * Fmt<F>::BN <= (F == FASTID_TENSOR_F4 ? (int)kSfaCol : Fmt<F>::kTmemCols), "TMEM columns");
     constexpr int BN = Fmt<F>::BN;
     constexpr int CPW = Fmt<F>::kCoresPerWord;
     // the mxf4 image is stored in the pair layout: each stage = two BN/2-row halves
@@ -268,15 +271,11 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     uint64_t* u_full = p_empty + kMaxPackedStages;
     uint64_t* u_empty = u_full + kMaxUnpackedStages;
     uint64_t* t_full = u_empty + kMaxUnpackedStages;
-    uint64_t* t_empty = t_full + 2;
-    uint64_t* a_full = t_empty + 2;
+    uint64_t* t_empty = t_full + kAccBufs;
+    uint64_t* a_full = t_empty + kAccBufs;
     uint64_t* ar_full = a_full + 1;  // streamed-A ring
     uint64_t* ar_empty = ar_full + kMaxAStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ar_empty + kMaxAStages);
-    // published top-k admission bounds [split][unknown]; only ever decrease, so a
-    // stale read is a looser (still correct) bound
-    volatile uint32_t* pub = reinterpret_cast<volatile uint32_t*>(smem + lay.off_bar + Layout<F>::kBarBytes);
-    for (int i = threadIdx.x; i < kMaxSplits * kM; i += blockDim.x) pub[i] = 0xFFFFFFFFu;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -298,7 +297,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             ptx::mbar_init(&u_full[i], IMG ? 1 : kConvThreads);
             ptx::mbar_init(&u_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAccBufs; ++i) {
             ptx::mbar_init(&t_full[i], 1);
             // pairs: one arrival per epilogue warp of both CTAs (on the leader's barrier)
             ptx::mbar_init(&t_empty[i], PAIR ? 2 * kEpiWarps : kEpiThreads);
@@ -410,13 +409,14 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
             for (int64_t t = t_begin; t < t_end; ++t, ++local) {
-                const int acc = local & 1;
+                const int acc = local % kAccBufs;
+                const uint32_t use = (uint32_t)(local / kAccBufs) & 1u;  // parity of this buffer's use
                 const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
                 if (tr) a.trace[local * kTrSlots + kTrMmaWait] = clock64();
                 if (PAIR)
-                    ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
+                    ptx::mbar_wait(&t_empty[acc], use ^ 1);
                 else
-                    ptx::mbar_wait(&t_empty[acc], ((local >> 1) & 1) ^ 1);
+                    ptx::mbar_wait(&t_empty[acc], use ^ 1);
                 if (tr) a.trace[local * kTrSlots + kTrMmaGo] = clock64();
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
@@ -577,30 +577,32 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         const uint64_t cap = (uint64_t)a.max_score + 1;  // admit v <= max_score
         uint32_t thr_bits = 0;  // own list: admit v < thr_bits (rows arrive in index order)
         if (MODE == kTopK) thr_bits = score_bits<F>(cap < kEmptyScore ? (uint32_t)cap : kEmptyScore);
-        // Admission bound shared by the splits of one unknown: a value worse than
-        // another split's k-th best cannot be in the union's top k (that split
-        // holds k values <= it, ties resolved by the merge), so each split admits
-        // v <= min over splits of their k-th best -- stored as bits + 1.
+        // Admission bound shared by every list of one unknown (all column splits of
+        // all slices, a.bound[q], raw score bits, admit v < bound): a value worse
+        // than some list's KP-th best cannot be in the union's top k (that list
+        // holds KP >= k values <= it; ties are resolved by the merge), so every
+        // list admits v <= the minimum published KP-th best, stored + 1 and
+        // lowered with atomicMin.  Bounds only decrease, so a stale read is a
+        // looser, still correct, bound.  The list itself holds raw bits (decoded
+        // at the store), so an insertion needs no float <-> int conversion.
+        const uint32_t cap_bits = thr_bits;
         uint32_t thr_eff = thr_bits;
+        const bool share = MODE == kTopK && a.bound != nullptr && q_ok;
         const uint32_t hit_bits = MODE == kThreshold ? score_bits<F>(a.threshold) : 0u;
-        uint32_t t_empty_leader[2] = {0u, 0u};
+        uint32_t t_empty_leader[kAccBufs] = {};
         if (PAIR) {
-            t_empty_leader[0] = ptx::mapa(&t_empty[0], 0);
-            t_empty_leader[1] = ptx::mapa(&t_empty[1], 0);
+#pragma unroll
+            for (int i = 0; i < kAccBufs; ++i) t_empty_leader[i] = ptx::mapa(&t_empty[i], 0);
         }
         int local = 0;
         for (int64_t t = t_begin; t < t_end; ++t, ++local) {
-            const int acc = local & 1;
-            ptx::mbar_wait(&t_full[acc], (local >> 1) & 1);
+            const int acc = local % kAccBufs;
+            // the shared bound is read before the wait so its latency hides behind it
+            const uint32_t shared_bound = share ? __ldcg(a.bound + q) : 0xFFFFFFFFu;
+            ptx::mbar_wait(&t_full[acc], (uint32_t)(local / kAccBufs) & 1u);
             const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
             if (tr) a.trace[local * kTrSlots + kTrEpi0 + ew] = clock64();
-            if (MODE == kTopK && kSplits > 1) {
-#pragma unroll
-                for (int s2 = 0; s2 < kSplits; ++s2) {
-                    const uint32_t b = pub[s2 * kM + m];
-                    if (b < thr_eff) thr_eff = b;
-                }
-            }
+            if (shared_bound < thr_eff) thr_eff = shared_bound;
             ptx::tc_fence_after();
             const int64_t r0 = t * BN + split * kCols;
             const int64_t rows_left = a.n_refs - r0;
@@ -626,7 +628,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 const uint32_t mn = min32(v);
                 if (MODE == kTopK) {
-                    if (mn < thr_eff) {
+                    if (mn < thr_eff && !(a.debug_flags & 16)) {
                         uint32_t cand = 0;
 #pragma unroll
                         for (int c = 0; c < kBatch; ++c) cand |= (v[c] < thr_eff ? 1u : 0u) << c;
@@ -636,11 +638,13 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                             cand &= cand - 1;
                             const uint32_t vc = pick32(v, c);
                             if (vc < thr_eff) {
-                                top.insert(decode_exact<F>(vc), (uint32_t)(rc + c));
-                                const uint64_t w = top.s[KP - 1] < cap ? top.s[KP - 1] : cap;
-                                thr_bits = score_bits<F>(w < kEmptyScore ? (uint32_t)w : kEmptyScore);
+                                top.insert_last(vc, (uint32_t)(rc + c));  // raw bits; rows ascend
+                                if ((a.debug_flags & 32) && a.trace && local < a.trace_tiles)  // insertion census
+                                    atomicAdd((unsigned long long*)&a.trace[(int64_t)a.trace_tiles * kTrSlots + local], 1ull);
+                                const uint32_t kth = top.s[KP - 1];
+                                thr_bits = kth < cap_bits ? kth : cap_bits;
                                 if (thr_bits < thr_eff) thr_eff = thr_bits;
-                                if (kSplits > 1) pub[split * kM + m] = thr_bits == 0xFFFFFFFFu ? thr_bits : thr_bits + 1;
+                                if (share && kth != kEmptyScore) atomicMin(a.bound + q, kth + 1u);
                             }
                         }
                     }
@@ -746,6 +750,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             }
         }
         if (MODE == kTopK && q_ok) {
+#pragma unroll
+            for (int i = 0; i < KP; ++i)
+                if (top.s[i] != kEmptyScore) top.s[i] = decode_exact<F>(top.s[i]);
             const int64_t off = (((int64_t)slice * kMaxSplits + split) * a.n_queries + q) * KP;
             top.store(a.part_scores + off, a.part_index + off, a.ref_base);
         }

@@ -8,9 +8,14 @@ from paper_1707_00516_b200 import _native
 L = _native.lib()
 scratch = torch.zeros(4096, dtype=torch.int32, device="cuda")
 src = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
-names = {8 + 128 + 4 + 256: "pair N=192 tiled walk", 8 + 128 + 4 + 256 + 64: "pair N=192 tiled walk commit/4",
-         8 + 128 + 4 + 256 + 512: "pair N=192 tiled walk wait/4", 8 + 128 + 4 + 256 + 512 + 64: "pair N=192 tiled walk wait+commit/4",
-         8 + 4 + 256 + 512 + 64: "pair N=224 tiled walk wait+commit/4"}
+B = 268
+names = {}
+for nflag, n in ((128, "N=192"), (1024, "N=144")):
+    for extra, nm in ((0, "plain"), (64 + 512, "wait+commit/4"), (64 + 512 + 2048, "wait+commit/8"),
+                      (64 + 512 + 4096, "wait+commit/4 3buf"), (64 + 512 + 2048 + 4096, "wait+commit/8 3buf")):
+        if nflag == 128 and extra & 4096:
+            continue
+        names[B + nflag + extra] = f"pair {n} tiled {nm}"
 for variant, name in names.items():
     best = 0
     for rep in range(4):

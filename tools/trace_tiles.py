@@ -1,4 +1,7 @@
-"""Per-tile timeline of CTA 0 of the top-k tensor kernel (fastid_debug_trace)."""
+"""Per-tile timeline of CTA 0 of the top-k tensor kernel (fastid_debug_trace).
+
+usage: trace_tiles.py [N_R] [N_Q] [L] [TILES]
+"""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -7,51 +10,48 @@ import paper_1707_00516_b200 as m
 from paper_1707_00516_b200 import _native
 from paper_1707_00516_b200.search import KnownDatabase
 
-n_r, n_q, L, tiles = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+n_r, n_q, L, tiles = (int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (20_000_000, 2048, 1024, 8000)))
 g = torch.Generator(device="cuda").manual_seed(0)
 r = torch.randint(-2**62, 2**62, (n_r, L // 64), dtype=torch.int64, device="cuda", generator=g)
 q = torch.randint(-2**62, 2**62, (n_q, L // 64), dtype=torch.int64, device="cuda", generator=g)
 db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation="tensor_f4")
+del r
 dq = m.DevicePanel.from_words(q, L)
+lib = _native.lib()
+lib.fastid_debug_flags(int(sys.argv[5]) if len(sys.argv) > 5 else 0)
 db.topk_device(dq, 16); torch.cuda.synchronize()
-buf = torch.zeros((tiles, 67), dtype=torch.int64, device="cuda")
-_native.lib().fastid_debug_trace(buf.data_ptr(), tiles)
+buf = torch.zeros((tiles * 68,), dtype=torch.int64, device="cuda")
+lib.fastid_debug_trace(buf.data_ptr(), tiles)
 db.topk_device(dq, 16); torch.cuda.synchronize()
-_native.lib().fastid_debug_trace(None, 0)
-t = buf.cpu().numpy().astype(np.int64)
-t0 = t[0, 0]
-print("tile  mma_wait  mma_go  mma_issued | epi_acq(min,max)  epi_rel(min,max) | epi_busy(max)")
-for i in range(0, tiles, max(1, tiles // 40)):
-    row = t[i] - t0
-    acq, rel = row[3:19], row[19:35]
-    print(f"{i:5d} {row[0]:9d} {row[1]:8d} {row[2]:10d} | {acq.min():8d} {acq.max():8d}  {rel.min():8d} {rel.max():8d} | {(rel - acq).max():6d}")
-d = np.diff(t[:, 1])
-print("median MMA tile period (cycles):", np.median(d[d > 0]) if len(d) else None)
-print("median MMA wait (go - wait):", np.median(t[:, 1] - t[:, 0]))
-print("median epilogue span (max rel - min acq):", np.median(t[:, 19:35].max(1) - t[:, 3:19].min(1)))
-print("median lag commit->epi acquire:", np.median(t[:, 3:19].min(1) - t[:, 2]))
-acq, b0l, b0d, rel = t[:, 3:19], t[:, 35:51], t[:, 51:67], t[:, 19:35]
-sl = slice(200, None)
-print("per-warp medians (cycles) over tiles 200..:")
-print("  acquire -> batch0 loaded:", np.median((b0l - acq)[sl], axis=0).astype(int).tolist())
-print("  batch0 loaded -> processed:", np.median((b0d - b0l)[sl], axis=0).astype(int).tolist())
-print("  batch0 processed -> release (batch1 loaded):", np.median((rel - b0d)[sl], axis=0).astype(int).tolist())
-print("  acquire spread (max-min):", int(np.median((acq.max(1) - acq.min(1))[sl])))
-
-# same run with the epilogue's TMEM loads switched off (results invalid; timing only)
-_native.lib().fastid_debug_flags(1)
-buf.zero_()
-_native.lib().fastid_debug_trace(buf.data_ptr(), tiles)
-db.topk_device(dq, 16); torch.cuda.synchronize()
-_native.lib().fastid_debug_trace(None, 0)
-_native.lib().fastid_debug_flags(0)
-t = buf.cpu().numpy().astype(np.int64)
-d = np.diff(t[:, 1])
-print("NO-TMEM-LOAD epilogue: median MMA tile period:", np.median(d[d > 0]),
-      "median issue span (issued-go):", np.median(t[:, 2] - t[:, 1]))
+lib.fastid_debug_trace(None, 0)
+full = buf.cpu().numpy().astype(np.int64)
+ins = full[tiles * 67:]
+t = full[:tiles * 67].reshape(tiles, 67)[200:]
+if ins.any():
+    print("insertions per tile index (all CTAs):", [int(ins[i]) for i in (0, 1, 2, 5, 10, 20, 50, 100, 200, 500, 1000, 2000, 4000, 7000) if i < tiles])
+    print("total insertions:", int(ins.sum()))
+acq, rel, ld, done = t[:, 3:19], t[:, 19:35], t[:, 35:51], t[:, 51:67]
+w = [i for i in range(16) if acq[:, i].any()]
+acq, rel, ld, done = acq[:, w], rel[:, w], ld[:, w], done[:, w]
+wait, go, issued = t[:, 0], t[:, 1], t[:, 2]
+med = lambda x: int(np.median(x))
+print(f"epilogue warps traced: {len(w)}")
+print(f"MMA tile period {med(np.diff(go))}; t_empty wait (go-wait) {med(go - wait)}; issue span {med(issued - go)}")
+print(f"commit(issued) -> first acquire {med(acq.min(1) - issued)}; -> last acquire {med(acq.max(1) - issued)}")
+print(f"acquire -> loaded (per warp median) {med(ld - acq)}; loaded -> processed {med(done - ld)}; release - loaded {med(rel - ld)}")
+print(f"last release of tile i -> MMA go of tile i+2 {med(go[2:] - rel.max(1)[:-2])}")
+print(f"per-warp processed(i) -> acquire(i+1) {med(acq[1:] - done[:-1])}")
+for pct in (50, 90, 99):
+    print(f"  p{pct}: loaded->processed {int(np.percentile(done - ld, pct))}, acquire spread {int(np.percentile(acq.max(1) - acq.min(1), pct))}")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for flags in (0, 1):
-    _native.lib().fastid_debug_flags(flags)
-    e0.record(); db.topk_device(dq, 16); e1.record(); e1.synchronize()
-    print(f"flags={flags}: kernel+merge {e0.elapsed_time(e1):.3f} ms")
-_native.lib().fastid_debug_flags(0)
+e0.record(); db.topk_device(dq, 16); e1.record(); e1.synchronize()
+print(f"kernel+merge {e0.elapsed_time(e1):.3f} ms")
+pt = done - ld
+for lo, hi in ((0, 200), (500, 700), (1100, 1300)):
+    x = pt[lo:hi]
+    print(f"tiles {lo+200}-{hi+200}: loaded->processed p50 {int(np.percentile(x, 50))} p90 {int(np.percentile(x, 90))} "
+          f"p99 {int(np.percentile(x, 99))}; MMA wait p50 {med((go - wait)[lo:hi])}")
+for lo in (2000, 4000, 7000):
+    x = pt[lo:lo + 500]
+    print(f"tiles {lo+200}-{lo+700}: loaded->processed p50 {int(np.percentile(x, 50))} p90 {int(np.percentile(x, 90))} "
+          f"p99 {int(np.percentile(x, 99))}; MMA wait p50 {med((go - wait)[lo:lo+500])}")
