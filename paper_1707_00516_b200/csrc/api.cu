@@ -215,7 +215,7 @@ extern "C" int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, i
     (void)formulation;
     // partial lists + one shared admission bound per unknown
     *bytes = (size_t)parts * (size_t)n_queries * (size_t)kp * (sizeof(uint32_t) + sizeof(int64_t)) +
-             (size_t)n_queries * sizeof(uint32_t) + 256;
+             (size_t)(n_queries + 4) * (1 + kMinSlots) * sizeof(uint32_t) + 256;
     return FASTID_OK;
 }
 
@@ -245,7 +245,10 @@ int topk_partials_impl(const void* refs, const void* image, int64_t n_refs, cons
     a.part_index = (int64_t*)(((uintptr_t)workspace + 15) & ~(uintptr_t)15);
     a.part_scores = (uint32_t*)(a.part_index + (size_t)parts * n_queries * kp);
     a.bound = a.part_scores + (size_t)parts * n_queries * kp;
-    FASTID_CUDA(cudaMemsetAsync(a.bound, 0xFF, (size_t)n_queries * sizeof(uint32_t), (cudaStream_t)stream));
+    a.list_min = a.bound + ((n_queries + 3) & ~(int64_t)3);  // 16-B aligned rows of kMinSlots
+    FASTID_CUDA(cudaMemsetAsync(a.bound, 0xFF, (size_t)(((n_queries + 3) & ~(int64_t)3) + n_queries * kMinSlots) *
+                                                   sizeof(uint32_t),
+                                (cudaStream_t)stream));
     int launched_parts = 0;
     if (int rc = launch(kTopK, a, f, &launched_parts, (cudaStream_t)stream)) return rc;
     if (launched_parts > parts) FASTID_FAIL(FASTID_E_INVALID, "internal: partition mismatch");

@@ -38,6 +38,7 @@ const char* get_error();
     } while (0)
 
 constexpr int kMaxTopK = 32;
+constexpr int kMinSlots = 32;  // lists per unknown that publish their best value (shared top-k bound)
 constexpr uint32_t kEmptyScore = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyLocal = 0xFFFFFFFFu;
 
@@ -133,6 +134,7 @@ struct CompareArgs {
     int64_t* part_index;
     int kpad;
     uint32_t* bound;        // [n_queries] shared top-k admission bound (formulation's raw score bits: admit v < bound), or null
+    uint32_t* list_min;     // [n_queries][kMinSlots] best value published by each of the first kMinSlots lists
     // threshold
     uint32_t threshold;
     int64_t ref_base;

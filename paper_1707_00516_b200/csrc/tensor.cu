@@ -179,6 +179,35 @@ __device__ __forceinline__ uint32_t core_off(int row, int col, int rows) {
     return (uint32_t)col * (uint32_t)(rows * 16) + (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u;
 }
 
+// k-th smallest of the kMinSlots published list minima of one unknown
+// (unpublished slots hold 0xFFFFFFFF): sorted insertion of each value into a
+// K-entry register list, every position updated in parallel.
+template <int K>
+__device__ __forceinline__ uint32_t kth_smallest_published(const uint32_t* mins, int k) {
+    uint32_t v[kMinSlots];
+#pragma unroll
+    for (int j = 0; j < kMinSlots / 4; ++j) {
+        const uint4 x = __ldcg(reinterpret_cast<const uint4*>(mins) + j);
+        v[4 * j] = x.x, v[4 * j + 1] = x.y, v[4 * j + 2] = x.z, v[4 * j + 3] = x.w;
+    }
+    uint32_t best[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) best[i] = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < kMinSlots; ++j) {
+        bool le[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) le[i] = best[i] <= v[j];
+#pragma unroll
+        for (int i = K - 1; i > 0; --i) best[i] = le[i] ? best[i] : (le[i - 1] ? v[j] : best[i - 1]);
+        best[0] = le[0] ? best[0] : v[j];
+    }
+    uint32_t r = best[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i) r = i < k ? best[i] : r;  // best[k - 1] with static indexing
+    return r;
+}
+
 template <int F>
 struct Layout {
     static constexpr int BN = Fmt<F>::BN;
@@ -588,6 +617,17 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         const uint32_t cap_bits = thr_bits;
         uint32_t thr_eff = thr_bits;
         const bool share = MODE == kTopK && a.bound != nullptr && q_ok;
+        // Second bound: every list also publishes its best value; the k-th smallest
+        // of those published minima belongs to k distinct rows, so the union's k-th
+        // best is no worse -- close to the true k-th best once the lists fill, where
+        // the min over lists of their KP-th best is far looser.  Recomputed only
+        // when this list's best improves (rare).
+        const int list_id = slice * kSplits + split;
+        const int n_lists = n_slices * kSplits;
+        const int n_pub = n_lists < kMinSlots ? n_lists : kMinSlots;
+        const bool pub_min = share && a.list_min != nullptr && list_id < kMinSlots && n_pub >= a.k;
+        // the k-th smallest published minimum is folded into a.bound by every list
+        // at tiles 1, 2, 4, ... and then every 256th (SIMT-parallel over lanes)
         const uint32_t hit_bits = MODE == kThreshold ? score_bits<F>(a.threshold) : 0u;
         uint32_t t_empty_leader[kAccBufs] = {};
         if (PAIR) {
@@ -602,6 +642,13 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             ptx::mbar_wait(&t_full[acc], (uint32_t)(local / kAccBufs) & 1u);
             const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
             if (tr) a.trace[local * kTrSlots + kTrEpi0 + ew] = clock64();
+            if (pub_min && (local & (local - 1)) == 0 || (pub_min && (local & 255) == 0)) {
+                const uint32_t kb = kth_smallest_published<KP>(a.list_min + (int64_t)q * kMinSlots, a.k);
+                if (kb != 0xFFFFFFFFu) {
+                    atomicMin(a.bound + q, kb + 1u);
+                    if (kb + 1u < thr_eff) thr_eff = kb + 1u;
+                }
+            }
             if (shared_bound < thr_eff) thr_eff = shared_bound;
             ptx::tc_fence_after();
             const int64_t r0 = t * BN + split * kCols;
@@ -638,7 +685,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                             cand &= cand - 1;
                             const uint32_t vc = pick32(v, c);
                             if (vc < thr_eff) {
+                                const bool new_best = vc < top.s[0];
                                 top.insert_last(vc, (uint32_t)(rc + c));  // raw bits; rows ascend
+                                if (pub_min && new_best) __stcg(a.list_min + (int64_t)q * kMinSlots + list_id, vc);
                                 if ((a.debug_flags & 32) && a.trace && local < a.trace_tiles)  // insertion census
                                     atomicAdd((unsigned long long*)&a.trace[(int64_t)a.trace_tiles * kTrSlots + local], 1ull);
                                 const uint32_t kth = top.s[KP - 1];
