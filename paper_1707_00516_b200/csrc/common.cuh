@@ -135,6 +135,9 @@ struct CompareArgs {
     int kpad;
     uint32_t* bound;        // [n_queries] shared top-k admission bound (formulation's raw score bits: admit v < bound), or null
     uint32_t* list_min;     // [n_queries][kMinSlots] best value published by each of the first kMinSlots lists
+    // CTA-pair kernel: per (slice, unknown group) tile progress, for drift control
+    int* progress;
+    int n_groups;
     // threshold
     uint32_t threshold;
     int64_t ref_base;

@@ -62,6 +62,7 @@ struct Roles {
 // the others, so an epilogue warp that runs late on one tile (top-k
 // insertions) does not stall the tensor pipe.
 constexpr int kAccBufs = 2;
+constexpr int kDriftTiles = 40;  // max lead of a pair over the slowest pair of its slice
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
 constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
 constexpr int kSmemLimit = 227 * 1024;
@@ -365,7 +366,27 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         // ---------------- TMA producer (whole warp; one elected lane issues) ----------------
         {
             Ring ra(SA ? lay.sa : 1), rp(SP > 0 ? SP : 1), ru(SU);
-            for (int64_t t = t_begin; t < t_end; ++t) {
+            // Pairs of one slice (same known tiles, different unknown groups) stay
+            // within kDriftTiles of each other so every tile half is fetched from
+            // HBM once and served to the other groups from L2: the leader's
+            // producer publishes its progress and waits (bounded) while it leads
+            // the slowest pair of its slice by more than that.
+            int* prog = (PAIR && leader && a.progress) ? a.progress + (int64_t)slice * a.n_groups : nullptr;
+            // The peers' counters are loaded at one check and consumed at the next,
+            // so their latency never stalls the operand stream.
+            int local_t = 0;
+            int peer = 0x7FFFFFFF;  // this lane's peer counter, in flight since the last check
+            for (int64_t t = t_begin; t < t_end; ++t, ++local_t) {
+                if (prog && (local_t & 7) == 0) {
+                    int lo = __reduce_min_sync(0xFFFFFFFFu, peer);
+                    for (int spin = 0; spin < 4096 && local_t - lo > kDriftTiles; ++spin) {
+                        __nanosleep(256);
+                        lo = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
+                        lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+                    }
+                    if (lane == 0) ptx::st_relaxed(prog + group, local_t);
+                    peer = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
+                }
                 for (int ks = 0; ks < n_kst; ++ks, rp.next()) {
                     if (SA) {
                         // this stage's slice of the pre-unpacked A operand (one bulk copy)
@@ -417,6 +438,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     __syncwarp();
                 }
             }
+            if (prog && lane == 0) ptx::st_relaxed(prog + group, 0x7FFFFFFF);  // finished: never waited on
         }
     } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer (the leader's warp for a pair; one elected lane issues) ----------------
@@ -959,7 +981,12 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
         FASTID_LAUNCHED("prep_a_kernel");
     }
     if (PAIR) {
-        const int64_t pairs = ceil_div(a.n_queries, 2 * kM) * n_slices;
+        const int64_t pgroups = ceil_div(a.n_queries, 2 * kM);
+        const int64_t pairs = pgroups * n_slices;
+        CompareArgs ap = a;
+        ap.n_groups = (int)pgroups;
+        FASTID_CUDA(cudaMallocAsync((void**)&ap.progress, (size_t)pairs * sizeof(int), stream));
+        FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)pairs * sizeof(int), stream));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(2 * pairs));
         cfg.blockDim = dim3(Roles<F, IMG>::kThreads);
@@ -972,7 +999,8 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a, (const uint8_t*)a_global, tiles, n_slices));
+        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, ap, (const uint8_t*)a_global, tiles, n_slices));
+        FASTID_CUDA(cudaFreeAsync(ap.progress, stream));
     } else {
         kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, a, a_global, tiles,
                                                                                          n_slices);

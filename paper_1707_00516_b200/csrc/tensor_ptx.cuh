@@ -78,6 +78,16 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// Relaxed gpu-scope global accesses (progress counters shared between CTAs).
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ---- clusters (CTA pairs for cta_group::2) ----------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;

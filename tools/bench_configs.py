@@ -33,10 +33,13 @@ def rand_words(n, L, gen, density=None):
     if density is None:
         w = torch.randint(-(2**63), 2**63 - 1, (n, nw), dtype=torch.int64, device="cuda", generator=gen)
     else:
-        bits = (torch.rand((n, nw * 64), device="cuda", generator=gen) < density).to(torch.int64)
         w = torch.zeros((n, nw), dtype=torch.int64, device="cuda")
-        for b in range(64):
-            w |= bits[:, b::64] << (63 - b)
+        step = max(1, (1 << 28) // (nw * 64))  # rows per chunk: ~1 GiB of float draws
+        for r0 in range(0, n, step):
+            bits = (torch.rand((min(step, n - r0), nw * 64), device="cuda", generator=gen) < density).to(torch.int64)
+            for b in range(64):
+                w[r0:r0 + bits.shape[0]] |= bits[:, b::64] << (63 - b)
+            del bits
     tail = L % 64
     if tail:
         w[:, -1] &= ~((1 << (64 - tail)) - 1)
