@@ -180,6 +180,8 @@ class ClockSampler:
         self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"fastid_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
+        if os.environ.get("FASTID_NO_CLOCKS"):  # diagnostics: run without the sampler
+            return self
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -371,6 +373,8 @@ def run_b200(args):
         clocks.mark(False)
     elapsed = ev0.elapsed_time(ev1) / 1e3
     kernel_s = [a.elapsed_time(b) / 1e3 for a, b in kern_ms]
+    if os.environ.get("FASTID_BENCH_STEPS"):
+        print("kernel ms per step:", [round(x * 1e3, 3) for x in kernel_s], file=sys.stderr)
     if world > 1:
         t = torch.tensor([elapsed, max(kernel_s)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -27,6 +27,11 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "tensor_ptx.cuh"
@@ -309,6 +314,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if ((a.debug_flags & 64) && a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 4] = (long long)ptx::globaltimer();
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // CTA pair or CTA
@@ -351,6 +357,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // debug flag 64: per-CTA %globaltimer stamps (entry, roles start, roles done, exit)
+    const bool cta_trace = (a.debug_flags & 64) && a.trace && threadIdx.x == 0;
+    if (cta_trace) a.trace[blockIdx.x * 4 + 1] = (long long)ptx::globaltimer();
     if (F == FASTID_TENSOR_F4 && warp >= kFirstEpiWarp && warp < kProducerWarp) {
         // unit block scales (ue8m0 127) for every MMA: whole SF region, all lanes
         const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
@@ -379,13 +388,17 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             for (int64_t t = t_begin; t < t_end; ++t, ++local_t) {
                 if (prog && (local_t & 7) == 0) {
                     int lo = __reduce_min_sync(0xFFFFFFFFu, peer);
-                    for (int spin = 0; spin < 4096 && local_t - lo > kDriftTiles; ++spin) {
+                    int spin = 0;
+                    for (; spin < 4096 && local_t - lo > kDriftTiles; ++spin) {
                         __nanosleep(256);
                         lo = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
                         lo = __reduce_min_sync(0xFFFFFFFFu, lo);
                     }
-                    if (lane == 0) ptx::st_relaxed(prog + group, local_t);
-                    peer = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
+                    if (lane == 0) ptx::st_relaxed(prog + group, spin == 4096 ? 0x7FFFFFFF : local_t);
+                    // a peer that stays ~1 ms behind is not co-resident (a shared GPU):
+                    // stop pacing rather than wait on it again
+                    if (spin == 4096) prog = nullptr;
+                    if (prog) peer = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
                 }
                 for (int ks = 0; ks < n_kst; ++ks, rp.next()) {
                     if (SA) {
@@ -438,7 +451,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     __syncwarp();
                 }
             }
-            if (prog && lane == 0) ptx::st_relaxed(prog + group, 0x7FFFFFFF);  // finished: never waited on
+            if (PAIR && leader && a.progress && lane == 0)
+                ptx::st_relaxed(a.progress + (int64_t)slice * a.n_groups + group, 0x7FFFFFFF);  // finished: never waited on
         }
     } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer (the leader's warp for a pair; one elected lane issues) ----------------
@@ -839,6 +853,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         }
     }
 
+    if (cta_trace) a.trace[blockIdx.x * 4 + 2] = (long long)ptx::globaltimer();
     ptx::tc_fence_before();
     if (PAIR)
         ptx::cluster_sync();  // the leader's MMAs and the peer's remote arrivals are all done
@@ -851,9 +866,47 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         else
             ptx::tmem_dealloc(tmem, Fmt<F>::kTmemCols);
     }
+    if (cta_trace) a.trace[blockIdx.x * 4 + 3] = (long long)ptx::globaltimer();
 }
 
 // ---- host side -------------------------------------------------------------
+
+// Launch scratch (pair progress counters, streamed-A operand) kept per
+// (device, stream) and grown on demand: stream-ordered reuse needs no
+// per-launch cudaMallocAsync, which costs ~250 us when the pool trims.
+void* launch_scratch(int which, size_t bytes, cudaStream_t stream) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& slot = cache[std::make_tuple(dev, stream, which)];
+    if (slot.second < bytes) {
+        if (slot.first) {
+            cudaStreamSynchronize(stream);  // the old buffer may still be in use on this stream
+            cudaFree(slot.first);
+        }
+        slot = {nullptr, 0};
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+        slot = {p, bytes};
+    }
+    return slot.first;
+}
+
+// Debug flag 128: host-side phase timings of a launch, printed to stderr.
+struct HostClock {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit HostClock(bool on_) : on(on_), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[fastid host] %-24s %8.1f us\n", what,
+                std::chrono::duration<double, std::micro>(n - t).count());
+        t = n;
+    }
+};
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -959,22 +1012,26 @@ int make_image_map(CUtensorMap* map, const CompareArgs& a) {
 
 template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
 int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
+    HostClock hc(a.debug_flags & 128);
     CUtensorMap map;
     if (PAIR) {
         if (int rc = make_image_map<F>(&map, a)) return rc;
     } else {
         if (int rc = make_known_map(&map, a, Fmt<F>::BN)) return rc;
     }
+    hc.mark("tensor map");
     const Layout<F> lay(a.stride, SA, IMG, PAIR);
     if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
     auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR>;
     FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
+    hc.mark("set attribute");
     const int64_t groups = ceil_div(a.n_queries, kM);
     const int64_t tiles = ceil_div(a.n_refs, Fmt<F>::BN);
     uint8_t* a_global = nullptr;
     if (SA) {
         const size_t bytes = (size_t)groups * lay.n_kst * Layout<F>::kAStageBytes;
-        FASTID_CUDA(cudaMallocAsync((void**)&a_global, bytes, stream));
+        a_global = (uint8_t*)launch_scratch(0, bytes, stream);
+        if (!a_global) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %zu bytes of streamed-A operand", bytes);
         const int64_t work = groups * lay.n_kst * kM;
         prep_a_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 16), 256, 0, stream>>>(
             a, (int)groups, lay.n_kst, a_global);
@@ -985,8 +1042,10 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
         const int64_t pairs = pgroups * n_slices;
         CompareArgs ap = a;
         ap.n_groups = (int)pgroups;
-        FASTID_CUDA(cudaMallocAsync((void**)&ap.progress, (size_t)pairs * sizeof(int), stream));
+        ap.progress = (int*)launch_scratch(1, (size_t)pairs * sizeof(int), stream);
+        if (!ap.progress) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the pair progress counters");
         FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)pairs * sizeof(int), stream));
+        hc.mark("progress alloc+memset");
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(2 * pairs));
         cfg.blockDim = dim3(Roles<F, IMG>::kThreads);
@@ -1000,13 +1059,12 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, ap, (const uint8_t*)a_global, tiles, n_slices));
-        FASTID_CUDA(cudaFreeAsync(ap.progress, stream));
+        hc.mark("cluster launch");
     } else {
         kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, a, a_global, tiles,
                                                                                          n_slices);
     }
     FASTID_LAUNCHED("tensor_kernel");
-    if (SA) FASTID_CUDA(cudaFreeAsync(a_global, stream));
     return FASTID_OK;
 }
 
