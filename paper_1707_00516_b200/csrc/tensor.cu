@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -229,9 +230,13 @@ struct Layout {
     bool img;
     int ub;       // operand-ring stage bytes: the whole tile, or this CTA's half of it in a pair
     int off_u, off_p, off_bar, total;
-    __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false, bool pair = false) {
+    int out_bytes;  // full-matrix TMA-store staging (image kernels): one [cols][32] u32 block per epilogue warp
+    int off_out;
+    __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false, bool pair = false,
+                               int stage_out = 0) {
         n_kst = (int)((stride + kStageBytesPacked - 1) / kStageBytesPacked);
         img = image;
+        out_bytes = stage_out;
         ub = pair ? kUnpackedStageBytes / 2 : kUnpackedStageBytes;
         sa = 0;
         if (!stream_a) {
@@ -246,7 +251,7 @@ struct Layout {
         }
     }
     __host__ __device__ void place() {
-        const int room = kSmemLimit - a_bytes - kBarBytes;
+        const int room = kSmemLimit - a_bytes - kBarBytes - out_bytes - (out_bytes ? 128 : 0);
         if (img) {
             // the tensor image is already in the UMMA layout: only the operand ring
             su = room / ub;
@@ -262,10 +267,20 @@ struct Layout {
         off_u = a_bytes;
         off_p = off_u + (su > 0 ? su : 0) * ub;
         off_bar = off_p + (sp > 0 ? sp : 0) * kPackedStageBytes;
-        total = off_bar + kBarBytes;
+        off_out = off_bar + kBarBytes;
+        off_out = (off_out + 127) & ~127;
+        total = off_out + out_bytes;
     }
     __host__ __device__ bool fits() const { return su >= 2 && (img || sp >= 2) && total <= kSmemLimit; }
 };
+
+// Full-matrix staging for TMA tensor stores (CTA-pair kernel): every epilogue
+// warp owns a [columns][32 unknowns] u32 block.
+template <int F, int MODE, bool IMG, bool PAIR>
+constexpr int out_stage_bytes() {
+    return (PAIR && MODE == kFull) ? Roles<F, IMG>::kEpiWarps * (Fmt<F>::BN / (Roles<F, IMG>::kEpiWarps / 4)) * 32 * 4
+                                   : 0;
+}
 
 // PAIR: a CTA pair (cluster of 2) issues cta_group::2 MMAs with M = 256 (each
 // CTA's 128 unknowns) and N = BN knowns, each CTA streaming only its half of
@@ -274,8 +289,8 @@ struct Layout {
 // The leader (rank 0) issues every MMA; the commits multicast to both CTAs.
 template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
 __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
-    tensor_kernel(const __grid_constant__ CUtensorMap tmap, CompareArgs a, const uint8_t* __restrict__ a_global,
-                  int64_t n_tiles, int n_slices) {
+    tensor_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap, CompareArgs a,
+                  const uint8_t* __restrict__ a_global, int64_t n_tiles, int n_slices) {
     static_assert(!PAIR || (F == FASTID_TENSOR_F4 && IMG && !SA), "pairs run the prepared mxf4 image only");
     static_assert(kAccBufs * Fmt<F>::BN <= (F == FASTID_TENSOR_F4 ? (int)kSfaCol : Fmt<F>::kTmemCols), "TMEM columns");
     constexpr int BN = Fmt<F>::BN;
@@ -292,7 +307,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     constexpr int kBuildWarps = R::kBuildWarps;
     constexpr int kFirstEpiWarp = R::kFirstEpiWarp, kProducerWarp = R::kProducerWarp, kMmaWarp = R::kMmaWarp;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const Layout<F> lay(a.stride, SA, IMG, PAIR);
+    const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0);
     constexpr int AB = Layout<F>::kAStageBytes;
     const int SP = lay.sp;
     const int SU = lay.su;
@@ -794,6 +809,26 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 release();
+                if (PAIR && MODE == kFull && a.tma_out) {
+                    // full matrix: transpose through this warp's staging block and let a
+                    // TMA tensor store write the [kCols known rows][32 unknowns] tile
+                    // (out-of-range rows / unknowns are clipped by the TMA unit)
+                    uint32_t* stage = reinterpret_cast<uint32_t*>(smem + lay.off_out) + ew * kCols * 32;
+                    if (lane == 0) ptx::bulk_wait_read0();  // the previous store has read the block
+                    __syncwarp();
+#pragma unroll
+                    for (int b = 0; b < kPreBatches; ++b)
+#pragma unroll
+                        for (int c = 0; c < kBatch; ++c)
+                            if (b * kBatch + c < kCols) stage[(b * kBatch + c) * 32 + lane] = decode_fast<F>(v[b][c]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&omap, stage, (int)(q0 + quad * 32), (int)r0);
+                        ptx::bulk_commit();
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int b = 0; b < kPreBatches; ++b) {
                     const int nb = kCols - b * kBatch < kBatch ? kCols - b * kBatch : kBatch;
@@ -834,6 +869,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 process(v, b0, nb);
             }
         }
+        if (PAIR && MODE == kFull && a.tma_out && lane == 0) ptx::bulk_wait_all();  // stores done before exit
         if (MODE == kTopK && q_ok) {
 #pragma unroll
             for (int i = 0; i < KP; ++i)
@@ -1010,9 +1046,35 @@ int make_image_map(CUtensorMap* map, const CompareArgs& a) {
     return FASTID_OK;
 }
 
+// Tensor map over the u32 full-matrix output [n_refs][ld_out] (inner dim =
+// unknowns): one box = one epilogue warp's [cols][32] block.  Needs 16-byte
+// alignment of the base and the row pitch.
+int make_out_map(CUtensorMap* map, const CompareArgs& a, int box_cols) {
+    auto fn = encode_fn();
+    if (!fn) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)a.n_queries, (cuuint64_t)a.n_refs};
+    cuuint64_t strides[1] = {(cuuint64_t)a.ld_out * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_cols};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)a.out, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled (output) failed (%d)", (int)r);
+    return FASTID_OK;
+}
+
 template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
-int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
-    HostClock hc(a.debug_flags & 128);
+int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) {
+    HostClock hc(a_in.debug_flags & 128);
+    CompareArgs a = a_in;
+    CUtensorMap omap;
+    memset(&omap, 0, sizeof(omap));
+    a.tma_out = 0;
+    if (PAIR && MODE == kFull && a.n_queries > 0 && ((uintptr_t)a.out & 15) == 0 && (a.ld_out * 4) % 16 == 0 &&
+        !(a.debug_flags & 256) && Layout<F>(a.stride, SA, IMG, PAIR, out_stage_bytes<F, MODE, IMG, PAIR>()).fits()) {
+        if (int rc = make_out_map(&omap, a, Fmt<F>::BN / (Roles<F, IMG>::kEpiWarps / 4))) return rc;
+        a.tma_out = 1;
+    }
     CUtensorMap map;
     if (PAIR) {
         if (int rc = make_image_map<F>(&map, a)) return rc;
@@ -1020,7 +1082,7 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
         if (int rc = make_known_map(&map, a, Fmt<F>::BN)) return rc;
     }
     hc.mark("tensor map");
-    const Layout<F> lay(a.stride, SA, IMG, PAIR);
+    const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0);
     if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
     auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR>;
     FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
@@ -1058,11 +1120,11 @@ int launch_one_impl(const CompareArgs& a, int n_slices, cudaStream_t stream) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, ap, (const uint8_t*)a_global, tiles, n_slices));
+        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, omap, ap, (const uint8_t*)a_global, tiles, n_slices));
         hc.mark("cluster launch");
     } else {
-        kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, a, a_global, tiles,
-                                                                                         n_slices);
+        kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, omap, a, a_global,
+                                                                                         tiles, n_slices);
     }
     FASTID_LAUNCHED("tensor_kernel");
     return FASTID_OK;

@@ -247,11 +247,14 @@ def test_prepared_database_image(rng, form, L):
 
 
 @pytest.mark.parametrize("pairs", [True, False])
-@pytest.mark.parametrize("shape", [(1137, 129, 1024), (2500, 520, 2048), (700, 300, 1800), (224, 256, 64)])
+@pytest.mark.parametrize("shape", [(1137, 129, 1024), (2500, 520, 2048), (700, 300, 1800), (224, 256, 64),
+                                   (3001, 388, 1024), (5000, 260, 512)])
 def test_image_pairs_and_split(rng, pairs, shape):
     """Prepared mxf4 image: the CTA-pair kernel (cta_group::2, M=256) and the
     single-CTA split-B kernel (debug flag 2) both equal the oracle, for every
-    epilogue, with ragged unknown groups and known tiles."""
+    epilogue, with ragged unknown groups and known tiles.  Unknown counts that
+    are multiples of 4 with L <= 1024 take the TMA-store full-matrix epilogue,
+    the others its direct-store fallback."""
     m = fb()
     from paper_1707_00516_b200 import _native
     from paper_1707_00516_b200.search import KnownDatabase
