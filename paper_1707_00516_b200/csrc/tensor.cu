@@ -46,7 +46,7 @@ constexpr int kWordsPerStage = kStageBytesPacked / 4;
 constexpr int kMaxPackedStages = 12;
 constexpr int kMinPackedStages = 4;
 constexpr int kMaxUnpackedStages = 8;
-constexpr int kMaxAStages = 4;
+constexpr int kMaxAStages = 8;
 // Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
 // highest warp ids (the scheduler favours higher ids), converters the lowest.
 // Packed operands: 8 converter warps (two per SMSP) + 8 epilogue warps.  A
@@ -289,9 +289,10 @@ constexpr int out_stage_bytes() {
 // The leader (rank 0) issues every MMA; the commits multicast to both CTAs.
 template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
 __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
-    tensor_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap, CompareArgs a,
-                  const uint8_t* __restrict__ a_global, int64_t n_tiles, int n_slices) {
-    static_assert(!PAIR || (F == FASTID_TENSOR_F4 && IMG && !SA), "pairs run the prepared mxf4 image only");
+    tensor_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                  const __grid_constant__ CUtensorMap amap, CompareArgs a, const uint8_t* __restrict__ a_global,
+                  int64_t n_tiles, int n_slices) {
+    static_assert(!PAIR || (F == FASTID_TENSOR_F4 && IMG), "pairs run the prepared mxf4 image only");
     static_assert(kAccBufs * Fmt<F>::BN <= (F == FASTID_TENSOR_F4 ? (int)kSfaCol : Fmt<F>::kTmemCols), "TMEM columns");
     constexpr int BN = Fmt<F>::BN;
     constexpr int CPW = Fmt<F>::kCoresPerWord;
@@ -421,9 +422,17 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         const int sa = ra.idx;
                         ptx::mbar_wait(&ar_empty[sa], ra.phase ^ 1);
                         if (ptx::elect_one()) {
-                            ptx::mbar_expect_tx(&ar_full[sa], AB);
-                            ptx::bulk_load(sA + sa * AB, a_global + ((int64_t)group * n_kst + ks) * AB, AB,
-                                           &ar_full[sa]);
+                            if (PAIR) {
+                                // each CTA streams its own 128 unknowns' stage; the leader's
+                                // barrier counts both
+                                if (leader) ptx::mbar_expect_tx(&ar_full[sa], 2 * AB);
+                                ptx::tma_load_2d_pair(sA + sa * AB, &amap, ptx::mapa(&ar_full[sa], 0), 0,
+                                                      (int)((((int64_t)group * 2 + rank) * n_kst + ks) * (AB / 128)));
+                            } else {
+                                ptx::mbar_expect_tx(&ar_full[sa], AB);
+                                ptx::bulk_load(sA + sa * AB, a_global + ((int64_t)group * n_kst + ks) * AB, AB,
+                                               &ar_full[sa]);
+                            }
                         }
                         __syncwarp();
                         ra.next();
@@ -519,6 +528,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                             ptx::mma_mxf4_pair_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol,
                                                       tmem + kSfbCol, ks ? 1u : 0u);
                             ptx::tc_commit_pair(&u_empty[s], 0x3);  // both halves of stage s reusable
+                            if (SA) ptx::tc_commit_pair(&ar_empty[sa], 0x3);
                         } else {
                             if (kSplitB)
                                 ptx::mma_mxf4_split_stage4(d, BN / 2, ad, bd, (uint64_t)(HB >> 4), a_step, b_step,
@@ -1063,6 +1073,24 @@ int make_out_map(CUtensorMap* map, const CompareArgs& a, int box_cols) {
     return FASTID_OK;
 }
 
+// Tensor map over the streamed-A operand ([group][stage][AB bytes], rows of
+// 128 B): one box = one stage of one 128-unknown group.
+template <int F>
+int make_a_map(CUtensorMap* map, const void* a_global, int64_t groups, int n_kst) {
+    auto fn = encode_fn();
+    if (!fn) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    constexpr int AB = Layout<F>::kAStageBytes;
+    cuuint64_t dims[2] = {128, (cuuint64_t)(groups * n_kst * (AB / 128))};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {128, (cuuint32_t)(AB / 128)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a_global, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled (A) failed (%d)", (int)r);
+    return FASTID_OK;
+}
+
 template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
 int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) {
     HostClock hc(a_in.debug_flags & 128);
@@ -1087,9 +1115,12 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR>;
     FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     hc.mark("set attribute");
-    const int64_t groups = ceil_div(a.n_queries, kM);
+    // pairs cover unknowns in groups of 256: prepare A for both halves of the last pair
+    const int64_t groups = PAIR ? 2 * ceil_div(a.n_queries, 2 * kM) : ceil_div(a.n_queries, kM);
     const int64_t tiles = ceil_div(a.n_refs, Fmt<F>::BN);
     uint8_t* a_global = nullptr;
+    CUtensorMap amap;
+    memset(&amap, 0, sizeof(amap));
     if (SA) {
         const size_t bytes = (size_t)groups * lay.n_kst * Layout<F>::kAStageBytes;
         a_global = (uint8_t*)launch_scratch(0, bytes, stream);
@@ -1098,6 +1129,9 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         prep_a_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 16), 256, 0, stream>>>(
             a, (int)groups, lay.n_kst, a_global);
         FASTID_LAUNCHED("prep_a_kernel");
+        if (PAIR) {
+            if (int rc = make_a_map<F>(&amap, a_global, groups, lay.n_kst)) return rc;
+        }
     }
     if (PAIR) {
         const int64_t pgroups = ceil_div(a.n_queries, 2 * kM);
@@ -1120,21 +1154,22 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, omap, ap, (const uint8_t*)a_global, tiles, n_slices));
+        FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, omap, amap, ap, (const uint8_t*)a_global, tiles, n_slices));
         hc.mark("cluster launch");
     } else {
-        kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, omap, a, a_global,
-                                                                                         tiles, n_slices);
+        kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, omap, amap, a,
+                                                                                         a_global, tiles, n_slices);
     }
     FASTID_LAUNCHED("tensor_kernel");
     return FASTID_OK;
 }
 
-// CTA pairs run the prepared mxf4 image with a resident unknown tile.
+// CTA pairs run the prepared mxf4 image, with a resident unknown tile when it
+// fits (L <= 2048) and a streamed one otherwise.
 template <int F>
 bool use_pair(const CompareArgs& a) {
     return F == FASTID_TENSOR_F4 && a.image != nullptr && !(a.debug_flags & 2) &&
-           Layout<F>(a.stride, false, true, true).fits();
+           (Layout<F>(a.stride, false, true, true).fits() || Layout<F>(a.stride, true, true, true).fits());
 }
 
 template <int F>
@@ -1153,7 +1188,11 @@ int launch_one(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     const bool sa = !Layout<F>(a.stride, false, img).fits();
     if (img) {
         if constexpr (F == FASTID_TENSOR_F4) {
-            if (use_pair<F>(a)) return launch_one_impl<F, MODE, KP, false, true, true>(a, n_slices, stream);
+            if (use_pair<F>(a)) {
+                if (Layout<F>(a.stride, false, true, true).fits())
+                    return launch_one_impl<F, MODE, KP, false, true, true>(a, n_slices, stream);
+                return launch_one_impl<F, MODE, KP, true, true, true>(a, n_slices, stream);
+            }
         }
         if (sa) return launch_one_impl<F, MODE, KP, true, true, false>(a, n_slices, stream);
         return launch_one_impl<F, MODE, KP, false, true, false>(a, n_slices, stream);

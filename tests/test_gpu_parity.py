@@ -248,7 +248,7 @@ def test_prepared_database_image(rng, form, L):
 
 @pytest.mark.parametrize("pairs", [True, False])
 @pytest.mark.parametrize("shape", [(1137, 129, 1024), (2500, 520, 2048), (700, 300, 1800), (224, 256, 64),
-                                   (3001, 388, 1024), (5000, 260, 512)])
+                                   (3001, 388, 1024), (5000, 260, 512), (1500, 300, 5000), (900, 520, 2304)])
 def test_image_pairs_and_split(rng, pairs, shape):
     """Prepared mxf4 image: the CTA-pair kernel (cta_group::2, M=256) and the
     single-CTA split-B kernel (debug flag 2) both equal the oracle, for every
