@@ -442,6 +442,9 @@ def run_b200(args):
         "unit": "TFLOP/s",
         "frac": achieved_tflops / peak["tflops"],
         "traffic": traffic,
+        "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/ncu_traffic.json)" if traffic else None,
+        "algorithmic_bytes": n_local * ((L + 255) // 256) * 256 // 2 + args.n_unknown * db.panel.stride
+        if formulation == "tensor_f4" else None,
         "peak_source": (f"measured on this box by fastid_probe_peak ({formulation} inner instruction only, one CTA "
                         f"per SM); 1 MAC = 1 bit-pair = 2 FLOP"),
         "kernel_ms": kern_avg * 1e3,
