@@ -1138,9 +1138,12 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         const int64_t pairs = pgroups * n_slices;
         CompareArgs ap = a;
         ap.n_groups = (int)pgroups;
-        ap.progress = (int*)launch_scratch(1, (size_t)pairs * sizeof(int), stream);
-        if (!ap.progress) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the pair progress counters");
-        FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)pairs * sizeof(int), stream));
+        ap.progress = nullptr;
+        if (2 * pairs <= num_sms()) {  // drift control only among co-resident pairs
+            ap.progress = (int*)launch_scratch(1, (size_t)pairs * sizeof(int), stream);
+            if (!ap.progress) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the pair progress counters");
+            FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)pairs * sizeof(int), stream));
+        }
         hc.mark("progress alloc+memset");
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(2 * pairs));

@@ -285,3 +285,38 @@ def test_image_pairs_and_split(rng, pairs, shape):
         assert np.array_equal(hits.score, hs)
     finally:
         lib.fastid_debug_flags(0)
+
+
+@pytest.mark.parametrize("k,max_score", [(5, None), (16, 240), (1, 250), (32, None)])
+def test_pairs_topk_caps_and_list_sizes(rng, k, max_score):
+    """CTA-pair top-k with list sizes 8/16/32, a score cap, and shared
+    admission bounds over many lists (25 slices x 3 splits per unknown)."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L, n_r, n_q = 1024, 4800, 512
+    r, _ = rand_words(rng, n_r, L // 64, 64, L)
+    q, _ = rand_words(rng, n_q, L // 64, 64, L)
+    q[::7] = r[rng.integers(0, n_r, len(q[::7]))]
+    db = KnownDatabase(r, L, formulation="tensor_f4")
+    s, x = db.search_words(q, k, max_score)
+    es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE if max_score is None else max_score)
+    assert np.array_equal(s, es) and np.array_equal(x, ex)
+
+
+def test_pairs_more_groups_than_sms(rng):
+    """More unknown groups than co-resident CTA pairs (drift control off; the
+    grid runs in waves): still exact."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L, n_r, n_q = 256, 1500, 80 * 256 + 37
+    r, _ = rand_words(rng, n_r, L // 64, 64, L)
+    q, _ = rand_words(rng, n_q, L // 64, 64, L)
+    db = KnownDatabase(r, L, formulation="tensor_f4")
+    s, x = db.search_words(q, 4)
+    pick = np.arange(0, n_q, 97)
+    es, ex, _ = oracle.topk(r, q[pick], 4)
+    assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex)
+    full = db.full_device(m.DevicePanel.from_words(q[:300], L)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, oracle.naive(r, q[:300]))
