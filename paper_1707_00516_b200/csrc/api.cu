@@ -1,8 +1,13 @@
 // C ABI entry points (include/fastid_b200.h): argument checks, formulation
 // dispatch, the top-k workspace protocol and the synchronous host-buffer
 // drop-in behind fastid_run_kernel.
+#include <condition_variable>
+#include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -82,16 +87,151 @@ int launch(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaS
 
 // ---- host-buffer context for fastid_run_kernel ------------------------------
 
+// A small fixed pool of host threads for parallel memcpy between pinned
+// staging and the caller's (pageable, possibly untouched) buffers: one
+// thread's memcpy into first-touched pages runs far below PCIe rate.
+class CopyPool {
+  public:
+    explicit CopyPool(int n) {
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    int size() const { return (int)workers_.size(); }
+    // memcpy(dst, src, bytes) split over the pool (caller participates); returns when done
+    void copy(void* dst, const void* src, size_t bytes) {
+        const int n = size() + 1;
+        if (bytes < ((size_t)4 << 20) || n == 1) {
+            memcpy(dst, src, bytes);
+            return;
+        }
+        const size_t part = ((bytes + n - 1) / n + 4095) & ~(size_t)4095;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = (char*)dst;
+            src_ = (const char*)src;
+            bytes_ = bytes;
+            part_ = part;
+            pending_ = size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        run_part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+  private:
+    void run_part(int i) {
+        const size_t lo = (size_t)i * part_;
+        if (lo >= bytes_) return;
+        const size_t hi = lo + part_ < bytes_ ? lo + part_ : bytes_;
+        memcpy(dst_ + lo, src_ + lo, hi - lo);
+    }
+    void loop(int i) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            lk.unlock();
+            run_part(i + 1);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    bool stop_ = false;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0, part_ = 0;
+};
+
 struct HostContext {
     int device = -1;
     cudaStream_t stream = nullptr;
     void* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // staging, refs, queries, out
     size_t cap[4] = {0, 0, 0, 0};
+    // chunked pipeline: pinned staging and device slots, double-buffered
+    void* pin_in[2] = {nullptr, nullptr};
+    void* pin_out[2] = {nullptr, nullptr};
+    size_t pin_in_cap = 0, pin_out_cap = 0;
+    void* dev_slot[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // raw, rows, out
+    size_t dev_slot_cap[3] = {0, 0, 0};
+    cudaEvent_t d2h_done[2] = {nullptr, nullptr};
+    cudaEvent_t h2d_done[2] = {nullptr, nullptr};
+    CopyPool* pool = nullptr;
 
     ~HostContext() {
         for (void* p : buf)
             if (p) cudaFree(p);
+        for (int i = 0; i < 2; ++i) {
+            if (pin_in[i]) cudaFreeHost(pin_in[i]);
+            if (pin_out[i]) cudaFreeHost(pin_out[i]);
+            for (void* p : dev_slot[i])
+                if (p) cudaFree(p);
+            if (d2h_done[i]) cudaEventDestroy(d2h_done[i]);
+            if (h2d_done[i]) cudaEventDestroy(h2d_done[i]);
+        }
+        delete pool;
         if (stream) cudaStreamDestroy(stream);
+    }
+    int ensure_pipeline(size_t in_bytes, size_t raw_bytes, size_t rows_bytes, size_t out_bytes) {
+        if (!pool) {
+            unsigned hc = std::thread::hardware_concurrency();
+            pool = new CopyPool((int)(hc > 2 ? (hc > 16 ? 15 : hc - 1) : 1));
+        }
+        for (int i = 0; i < 2; ++i) {
+            if (!d2h_done[i] && cudaEventCreateWithFlags(&d2h_done[i], cudaEventDisableTiming) != cudaSuccess)
+                FASTID_FAIL(FASTID_E_CUDA, "cudaEventCreate failed");
+            if (!h2d_done[i] && cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming) != cudaSuccess)
+                FASTID_FAIL(FASTID_E_CUDA, "cudaEventCreate failed");
+        }
+        if (in_bytes > pin_in_cap || out_bytes > pin_out_cap) {
+            cudaStreamSynchronize(stream);
+            for (int i = 0; i < 2; ++i) {
+                if (in_bytes > pin_in_cap) {
+                    if (pin_in[i]) cudaFreeHost(pin_in[i]);
+                    pin_in[i] = nullptr;
+                    if (cudaMallocHost(&pin_in[i], in_bytes) != cudaSuccess)
+                        FASTID_FAIL(FASTID_E_NOMEM, "cudaMallocHost of %zu bytes failed", in_bytes);
+                }
+                if (out_bytes > pin_out_cap) {
+                    if (pin_out[i]) cudaFreeHost(pin_out[i]);
+                    pin_out[i] = nullptr;
+                    if (cudaMallocHost(&pin_out[i], out_bytes) != cudaSuccess)
+                        FASTID_FAIL(FASTID_E_NOMEM, "cudaMallocHost of %zu bytes failed", out_bytes);
+                }
+            }
+            if (in_bytes > pin_in_cap) pin_in_cap = in_bytes;
+            if (out_bytes > pin_out_cap) pin_out_cap = out_bytes;
+        }
+        const size_t want[3] = {raw_bytes, rows_bytes, out_bytes};
+        for (int j = 0; j < 3; ++j) {
+            if (want[j] <= dev_slot_cap[j]) continue;
+            cudaStreamSynchronize(stream);
+            for (int i = 0; i < 2; ++i) {
+                if (dev_slot[i][j]) cudaFree(dev_slot[i][j]);
+                dev_slot[i][j] = nullptr;
+                if (cudaMalloc(&dev_slot[i][j], want[j]) != cudaSuccess) {
+                    cudaGetLastError();
+                    FASTID_FAIL(FASTID_E_NOMEM, "cudaMalloc of %zu bytes failed", want[j]);
+                }
+            }
+            dev_slot_cap[j] = want[j];
+        }
+        return FASTID_OK;
     }
     int ensure(int slot, size_t bytes) {
         if (bytes <= cap[slot]) return FASTID_OK;
@@ -108,6 +248,8 @@ struct HostContext {
 };
 
 thread_local HostContext* g_host_ctx = nullptr;
+constexpr size_t kPipelineMinBytes = (size_t)64 << 20;  // outputs above this stream through the chunk pipeline
+constexpr size_t kChunkOutBytes = (size_t)64 << 20;     // u32 output bytes per chunk
 
 int host_context(HostContext** out) {
     int dev = 0;
@@ -423,10 +565,13 @@ extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
     const int64_t stride = row_stride_bytes(bit_length);
     const size_t ref_in = (size_t)n_refs * row_bytes, q_in = (size_t)n_queries * row_bytes;
     const size_t out_bytes = (size_t)n_refs * n_queries * 4;
-    if (int rc = ctx->ensure(0, ref_in > q_in ? ref_in : q_in)) return rc;
-    if (int rc = ctx->ensure(1, (size_t)n_refs * stride)) return rc;
+    const bool chunked = out_bytes > kPipelineMinBytes;
+    if (int rc = ctx->ensure(0, chunked ? q_in : (ref_in > q_in ? ref_in : q_in))) return rc;
+    if (!chunked)
+        if (int rc = ctx->ensure(1, (size_t)n_refs * stride)) return rc;
     if (int rc = ctx->ensure(2, (size_t)n_queries * stride)) return rc;
-    if (int rc = ctx->ensure(3, out_bytes)) return rc;
+    if (!chunked)
+        if (int rc = ctx->ensure(3, out_bytes)) return rc;
     cudaStream_t st = ctx->stream;
     // queries first (the staging buffer is reused for the refs)
     FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], query_words, q_in, cudaMemcpyHostToDevice, st));
@@ -437,6 +582,47 @@ extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
         FASTID_LAUNCHED("transpose_words_kernel");
     } else if (int rc = fastid_load_words(ctx->buf[0], n_queries, row_bytes, ctx->buf[2], stride, st)) {
         return rc;
+    }
+    if (chunked) {
+        // Chunked pipeline over known rows (the paper's pinned-memory, overlapped
+        // transfer design, section IV-C; the reference's stage-in / compute /
+        // stage-out lanes, scheduler.py:270-419): while the GPU encodes, compares
+        // and copies chunk i into pinned slot i%2, the host threads move chunk i-1
+        // from its pinned slot into the caller's `out`.
+        const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n_refs, (int64_t)(kChunkOutBytes / ((size_t)n_queries * 4))));
+        const size_t cin = (size_t)rows * row_bytes, cout = (size_t)rows * n_queries * 4;
+        if (int rc = ctx->ensure_pipeline(cin, cin, (size_t)rows * stride, cout)) return rc;
+        const int64_t n_chunks = ceil_div(n_refs, rows);
+        auto drain = [&](int64_t c) -> int {  // host side of chunk c: pinned slot -> out
+            const int slot = (int)(c & 1);
+            const int64_t r0 = c * rows, nr = std::min<int64_t>(rows, n_refs - r0);
+            FASTID_CUDA(cudaEventSynchronize(ctx->d2h_done[slot]));
+            ctx->pool->copy((char*)out + (size_t)r0 * n_queries * 4, ctx->pin_out[slot], (size_t)nr * n_queries * 4);
+            return FASTID_OK;
+        };
+        for (int64_t c = 0; c < n_chunks; ++c) {
+            const int slot = (int)(c & 1);
+            const int64_t r0 = c * rows, nr = std::min<int64_t>(rows, n_refs - r0);
+            // the slot's previous upload has been consumed before its pinned input is rewritten
+            FASTID_CUDA(cudaEventSynchronize(ctx->h2d_done[slot]));
+            ctx->pool->copy(ctx->pin_in[slot], (const char*)ref_words + (size_t)r0 * row_bytes, (size_t)nr * row_bytes);
+            FASTID_CUDA(cudaMemcpyAsync(ctx->dev_slot[slot][0], ctx->pin_in[slot], (size_t)nr * row_bytes,
+                                        cudaMemcpyHostToDevice, st));
+            FASTID_CUDA(cudaEventRecord(ctx->h2d_done[slot], st));
+            if (int rc = fastid_load_words(ctx->dev_slot[slot][0], nr, row_bytes, ctx->dev_slot[slot][1], stride, st))
+                return rc;
+            if (int rc = fastid_compare_full(ctx->dev_slot[slot][1], nr, ctx->buf[2], n_queries, stride, bit_length,
+                                             (uint32_t*)ctx->dev_slot[slot][2], n_queries, formulation, st))
+                return rc;
+            FASTID_CUDA(cudaMemcpyAsync(ctx->pin_out[slot], ctx->dev_slot[slot][2], (size_t)nr * n_queries * 4,
+                                        cudaMemcpyDeviceToHost, st));
+            FASTID_CUDA(cudaEventRecord(ctx->d2h_done[slot], st));
+            if (c > 0)
+                if (int rc = drain(c - 1)) return rc;
+        }
+        if (int rc = drain(n_chunks - 1)) return rc;
+        FASTID_CUDA(cudaStreamSynchronize(st));
+        return FASTID_OK;
     }
     FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], ref_words, ref_in, cudaMemcpyHostToDevice, st));
     if (int rc = fastid_load_words(ctx->buf[0], n_refs, row_bytes, ctx->buf[1], stride, st)) return rc;

@@ -150,6 +150,21 @@ def test_run_kernel_host_path(rng, form):
         assert np.array_equal(out, oracle.naive(r, q))
 
 
+@pytest.mark.parametrize("width,transposed", [(64, False), (32, True)])
+def test_run_kernel_chunked_pipeline(rng, width, transposed):
+    """Outputs above 64 MB stream through the chunked pinned pipeline of
+    fastid_run_kernel (two chunks, the second ragged): every cell written."""
+    m = fb()
+    n_r, n_q, L = 45_000, 520, 512
+    r, _ = rand_words(rng, n_r, L // width, width)
+    q, _ = rand_words(rng, n_q, L // width, width)
+    out = np.empty((n_r, n_q), np.uint32)
+    qa = np.ascontiguousarray(q.T) if transposed else q
+    m.run_b200_kernel(r, qa, out, queries_transposed=transposed)
+    assert out.nbytes > 64 << 20
+    assert np.array_equal(out, oracle.naive(r, q))
+
+
 def test_executor_seam(rng):
     m = fb()
     r, _ = rand_words(rng, 100, 4, 64)
