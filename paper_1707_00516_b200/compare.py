@@ -264,9 +264,20 @@ def compare_b200(refs, queries, formulation: str | int = "auto", device=None) ->
     if n_r == 0 or n_q == 0:
         return ScoreMatrix(ref_ids, q_ids, np.zeros((n_r, n_q), dtype=np.uint32))
     dev = _require_cuda(device)
+    if n_r * n_q * 4 > _PIPELINE_MIN_BYTES and isinstance(refs.words, np.ndarray) \
+            and isinstance(queries.words, np.ndarray):
+        # large host results stream through the chunked pinned pipeline of the
+        # host-buffer ABI instead of one device-sized matrix and a pageable copy
+        scores = np.empty((n_r, n_q), np.uint32)
+        with torch.cuda.device(dev):
+            run_b200_kernel(refs.words, queries.words, scores, formulation=formulation)
+        return ScoreMatrix(ref_ids, q_ids, scores)
     d = compare_device(_as_device(refs, dev), _as_device(queries, dev), formulation=formulation)
     scores = d.cpu().numpy().view(np.uint32)
     return ScoreMatrix(ref_ids, q_ids, scores)
+
+
+_PIPELINE_MIN_BYTES = 64 << 20  # fastid_run_kernel streams outputs above this (csrc/api.cu)
 
 
 def compare_blocked_b200(refs, queries: QueryLayout, tile: TileConfig | None = None, parallelism: int = 1,

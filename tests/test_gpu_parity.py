@@ -165,6 +165,19 @@ def test_run_kernel_chunked_pipeline(rng, width, transposed):
     assert np.array_equal(out, oracle.naive(r, q))
 
 
+def test_compare_b200_large_result(rng):
+    """compare_b200 (the compare_naive drop-in) with a > 64 MB ScoreMatrix takes
+    the chunked host pipeline; u32 panels, partial last word."""
+    m = fb()
+    n_r, n_q, L = 33_000, 600, 1000
+    r, _ = rand_words(rng, n_r, -(-L // 32), 32, L)
+    q, _ = rand_words(rng, n_q, -(-L // 32), 32, L)
+    R, Q = m.Panel(tuple(range(n_r)), r, L), m.Panel(tuple(range(n_q)), q, L)
+    got = m.compare_b200(R, Q)
+    assert got.scores.nbytes > 64 << 20
+    assert np.array_equal(got.scores, oracle.naive(r, q))
+
+
 def test_executor_seam(rng):
     m = fb()
     r, _ = rand_words(rng, 100, 4, 64)
