@@ -172,6 +172,17 @@ FASTID_API int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
                       int64_t n_queries, int64_t n_words, int word_bits, int queries_transposed,
                       uint32_t* out, int formulation);
 
+/* The same comparison with the u32 rows appended, in row order, to the open
+ * file descriptor `fd` instead of a host array -- the payload of the
+ * reference's FIDM score file (BinaryScoreSink.put, io.py:244-255; the caller
+ * writes the 21-byte header, io.py:29-31).  The rows land at the
+ * descriptor's current offset (which must be seekable) via parallel
+ * pwrite(2) straight from pinned staging; on return the offset is past the
+ * last row.  Synchronous. */
+FASTID_API int fastid_run_kernel_fd(const void* ref_words, int64_t n_refs, const void* query_words,
+                                    int64_t n_queries, int64_t n_words, int word_bits, int queries_transposed,
+                                    int fd, int formulation);
+
 /* ---- measurement ------------------------------------------------------- */
 
 /* Pipe-peak probe (roofline denominator): launches an MMA-only (tensor

@@ -15,6 +15,7 @@ from .compare import (
     compare_b200,
     compare_blocked_b200,
     compare_device,
+    compare_to_fidm,
     row_stride,
     run_b200_kernel,
     threshold_hits,
@@ -51,7 +52,7 @@ __all__ = [
     "B200Executor", "CapacityError", "CodecError", "CorruptProfileError", "DeviceError",
     "DevicePanel", "FastIdError", "InfeasiblePlanError", "Panel", "PanelFormatError",
     "PanelMismatchError", "PipelineAbortError", "QueryLayout", "ScoreMatrix", "ThresholdHits",
-    "TileConfig", "TopKResult", "compare_b200", "compare_blocked_b200", "compare_device",
+    "TileConfig", "TopKResult", "compare_b200", "compare_blocked_b200", "compare_device", "compare_to_fidm",
     "relayout_queries", "restore_queries", "row_stride", "run_b200_kernel", "threshold_hits",
     "topk", "topk_device", "word_dtype", "words_per_profile",
 ]

@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
             "fastid_compare_threshold": ([vp, i64, vp, i64, i64, i64, u32, i64, vp, vp, vp, i64, vp, i32, vp], i32),
             "fastid_merge_topk": ([vp, vp, i32, i64, i32, i32, vp, vp, vp], i32),
             "fastid_run_kernel": ([vp, i64, vp, i64, i64, i32, i32, vp, i32], i32),
+            "fastid_run_kernel_fd": ([vp, i64, vp, i64, i64, i32, i32, i32, i32], i32),
             "fastid_db_image_bytes": ([i64, i64, i32], sz),
             "fastid_db_create": ([vp, i64, i64, i64, i32, vp, ctypes.POINTER(vp)], i32),
             "fastid_db_destroy": ([vp], i32),

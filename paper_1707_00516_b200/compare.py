@@ -28,6 +28,8 @@ the library is missing or no GPU is present the call raises.
 from __future__ import annotations
 
 import ctypes
+import os
+import struct
 
 import numpy as np
 import torch
@@ -319,6 +321,42 @@ def run_b200_kernel(ref_words: np.ndarray, query_words: np.ndarray, out: np.ndar
         ref_words.ctypes.data, n_refs, query_words.ctypes.data, n_q, n_words, ref_words.dtype.itemsize * 8,
         int(bool(queries_transposed)), out.ctypes.data, _native.formulation_code(formulation)),
         "fastid_run_kernel")
+
+
+FIDM_MAGIC = b"FIDM"
+FIDM_VERSION = 1
+_FIDM_HEADER = struct.Struct("<4sBQQ")  # io.py:29-31: magic, version, N_R, N_Q (little-endian)
+
+
+def compare_to_fidm(refs, queries, path, formulation: str | int = "auto", device=None) -> tuple[int, int]:
+    """Score ``refs`` x ``queries`` straight into a packed-binary score file.
+
+    Byte-identical to the reference's ``write_scores(compare_naive(refs, queries),
+    ScoreOutput(path, "binary"))`` / ``BinaryScoreSink`` (io.py:160-172, 244-255):
+    the "FIDM" header, then N_R x N_Q little-endian u32 cells in row order.  The
+    rows stream from the device through pinned staging to the file in chunks
+    (fastid_run_kernel_fd), never materialising the matrix in host memory.  A
+    partial file is removed if scoring fails, as the reference's sinks do.
+    Returns the matrix shape.
+    """
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    rw, qw = np.ascontiguousarray(refs.words), np.ascontiguousarray(queries.words)
+    n_r, n_q = rw.shape[0], qw.shape[0]
+    dev = _require_cuda(device) if n_r and n_q else None
+    with open(path, "wb") as fh:
+        try:
+            fh.write(_FIDM_HEADER.pack(FIDM_MAGIC, FIDM_VERSION, n_r, n_q))
+            fh.flush()
+            if n_r and n_q:
+                with torch.cuda.device(dev):
+                    _native.check(_native.lib().fastid_run_kernel_fd(
+                        rw.ctypes.data, n_r, qw.ctypes.data, n_q, rw.shape[1], rw.dtype.itemsize * 8, 0,
+                        fh.fileno(), _native.formulation_code(formulation)), "fastid_run_kernel_fd")
+        except BaseException:
+            fh.close()
+            os.unlink(path)
+            raise
+    return n_r, n_q
 
 
 class B200Executor:

@@ -1,6 +1,10 @@
 // C ABI entry points (include/fastid_b200.h): argument checks, formulation
 // dispatch, the top-k workspace protocol and the synchronous host-buffer
 // drop-in behind fastid_run_kernel.
+#include <unistd.h>
+
+#include <atomic>
+#include <cerrno>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -104,18 +108,18 @@ class CopyPool {
         for (auto& t : workers_) t.join();
     }
     int size() const { return (int)workers_.size(); }
-    // memcpy(dst, src, bytes) split over the pool (caller participates); returns when done
-    void copy(void* dst, const void* src, size_t bytes) {
+    // fn(lo, hi) over [0, bytes) split in page-aligned parts across the pool
+    // (the caller takes part 0); returns when every part is done
+    void parallel(size_t bytes, const std::function<void(size_t, size_t)>& fn) {
         const int n = size() + 1;
         if (bytes < ((size_t)4 << 20) || n == 1) {
-            memcpy(dst, src, bytes);
+            fn(0, bytes);
             return;
         }
         const size_t part = ((bytes + n - 1) / n + 4095) & ~(size_t)4095;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            dst_ = (char*)dst;
-            src_ = (const char*)src;
+            fn_ = &fn;
             bytes_ = bytes;
             part_ = part;
             pending_ = size();
@@ -126,13 +130,16 @@ class CopyPool {
         std::unique_lock<std::mutex> lk(mu_);
         done_.wait(lk, [this] { return pending_ == 0; });
     }
+    void copy(void* dst, const void* src, size_t bytes) {
+        parallel(bytes, [&](size_t lo, size_t hi) { memcpy((char*)dst + lo, (const char*)src + lo, hi - lo); });
+    }
 
   private:
     void run_part(int i) {
         const size_t lo = (size_t)i * part_;
         if (lo >= bytes_) return;
         const size_t hi = lo + part_ < bytes_ ? lo + part_ : bytes_;
-        memcpy(dst_ + lo, src_ + lo, hi - lo);
+        (*fn_)(lo, hi);
     }
     void loop(int i) {
         uint64_t seen = 0;
@@ -153,8 +160,7 @@ class CopyPool {
     bool stop_ = false;
     uint64_t gen_ = 0;
     int pending_ = 0;
-    char* dst_ = nullptr;
-    const char* src_ = nullptr;
+    const std::function<void(size_t, size_t)>* fn_ = nullptr;
     size_t bytes_ = 0, part_ = 0;
 };
 
@@ -551,9 +557,11 @@ extern "C" int fastid_db_compare_threshold(const fastid_db* db, const void* quer
                           ref_base, hit_query, hit_ref, hit_score, capacity, hit_count, db->formulation, stream);
 }
 
-extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries,
-                                 int64_t n_words, int word_bits, int queries_transposed, uint32_t* out,
-                                 int formulation) {
+namespace {
+// Host-buffer comparison: `out` (host, n_refs x n_queries u32) or, when fd >= 0,
+// the same rows appended to file descriptor fd (the FIDM payload).
+int run_host(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries, int64_t n_words,
+             int word_bits, int queries_transposed, uint32_t* out, int fd, int formulation) {
     if (word_bits != 32 && word_bits != 64) FASTID_FAIL(FASTID_E_INVALID, "word_bits must be 32 or 64");
     if (n_words <= 0 || n_refs < 0 || n_queries < 0) FASTID_FAIL(FASTID_E_INVALID, "bad panel shape");
     if (n_refs == 0 || n_queries == 0) return FASTID_OK;
@@ -565,7 +573,7 @@ extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
     const int64_t stride = row_stride_bytes(bit_length);
     const size_t ref_in = (size_t)n_refs * row_bytes, q_in = (size_t)n_queries * row_bytes;
     const size_t out_bytes = (size_t)n_refs * n_queries * 4;
-    const bool chunked = out_bytes > kPipelineMinBytes;
+    const bool chunked = out_bytes > kPipelineMinBytes || fd >= 0;
     if (int rc = ctx->ensure(0, chunked ? q_in : (ref_in > q_in ? ref_in : q_in))) return rc;
     if (!chunked)
         if (int rc = ctx->ensure(1, (size_t)n_refs * stride)) return rc;
@@ -593,11 +601,34 @@ extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
         const size_t cin = (size_t)rows * row_bytes, cout = (size_t)rows * n_queries * 4;
         if (int rc = ctx->ensure_pipeline(cin, cin, (size_t)rows * stride, cout)) return rc;
         const int64_t n_chunks = ceil_div(n_refs, rows);
+        // rows land at the descriptor's current offset (after the caller's header)
+        const off_t fd_base = fd >= 0 ? ::lseek(fd, 0, SEEK_CUR) : 0;
+        if (fd >= 0 && fd_base < 0) FASTID_FAIL(FASTID_E_INVALID, "fd %d is not seekable", fd);
         auto drain = [&](int64_t c) -> int {  // host side of chunk c: pinned slot -> out
             const int slot = (int)(c & 1);
             const int64_t r0 = c * rows, nr = std::min<int64_t>(rows, n_refs - r0);
             FASTID_CUDA(cudaEventSynchronize(ctx->d2h_done[slot]));
-            ctx->pool->copy((char*)out + (size_t)r0 * n_queries * 4, ctx->pin_out[slot], (size_t)nr * n_queries * 4);
+            const size_t nb = (size_t)nr * n_queries * 4;
+            if (fd < 0) {
+                ctx->pool->copy((char*)out + (size_t)r0 * n_queries * 4, ctx->pin_out[slot], nb);
+                return FASTID_OK;
+            }
+            // straight from the pinned slot to the file (parallel pwrite at the
+            // chunk's offset): no intermediate host copy
+            const off_t base = fd_base + (off_t)r0 * n_queries * 4;
+            std::atomic<int> err{0};
+            ctx->pool->parallel(nb, [&](size_t lo, size_t hi) {
+                for (size_t done = lo; done < hi;) {
+                    const ssize_t w = ::pwrite(fd, (const char*)ctx->pin_out[slot] + done, hi - done, base + (off_t)done);
+                    if (w < 0) {
+                        if (errno == EINTR) continue;
+                        err = errno;
+                        return;
+                    }
+                    done += (size_t)w;
+                }
+            });
+            if (err) FASTID_FAIL(FASTID_E_INVALID, "write to fd %d failed: %s", fd, strerror(err.load()));
             return FASTID_OK;
         };
         for (int64_t c = 0; c < n_chunks; ++c) {
@@ -622,6 +653,8 @@ extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
         }
         if (int rc = drain(n_chunks - 1)) return rc;
         FASTID_CUDA(cudaStreamSynchronize(st));
+        if (fd >= 0 && ::lseek(fd, fd_base + (off_t)out_bytes, SEEK_SET) < 0)
+            FASTID_FAIL(FASTID_E_INVALID, "lseek on fd %d failed", fd);
         return FASTID_OK;
     }
     FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], ref_words, ref_in, cudaMemcpyHostToDevice, st));
@@ -632,4 +665,21 @@ extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const vo
     FASTID_CUDA(cudaMemcpyAsync(out, ctx->buf[3], out_bytes, cudaMemcpyDeviceToHost, st));
     FASTID_CUDA(cudaStreamSynchronize(st));
     return FASTID_OK;
+}
+}  // namespace
+
+extern "C" int fastid_run_kernel(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries,
+                                 int64_t n_words, int word_bits, int queries_transposed, uint32_t* out,
+                                 int formulation) {
+    if (!out && n_refs > 0 && n_queries > 0) FASTID_FAIL(FASTID_E_INVALID, "out is NULL");
+    return run_host(ref_words, n_refs, query_words, n_queries, n_words, word_bits, queries_transposed, out, -1,
+                    formulation);
+}
+
+extern "C" int fastid_run_kernel_fd(const void* ref_words, int64_t n_refs, const void* query_words,
+                                    int64_t n_queries, int64_t n_words, int word_bits, int queries_transposed,
+                                    int fd, int formulation) {
+    if (fd < 0) FASTID_FAIL(FASTID_E_INVALID, "bad file descriptor %d", fd);
+    return run_host(ref_words, n_refs, query_words, n_queries, n_words, word_bits, queries_transposed, nullptr, fd,
+                    formulation);
 }

@@ -20,7 +20,10 @@ reference tree) and records, for a set of seeded inputs:
 * checksums.json    -- ``bench.score_checksum`` (bench.py:57-58) of
                        ``compare_blocked`` on ``synth_panel`` inputs
                        (bench.py:41-54), incl. BASELINE config 1;
-* genotype.json     -- ``codec.encode_genotype`` examples (codec.py:99-115).
+* genotype.json     -- ``codec.encode_genotype`` examples (codec.py:99-115);
+* fidm_cases.npz    -- panels and the packed-binary score files the reference's
+                       own ``io.write_scores(..., ScoreOutput(path, "binary"))``
+                       writes for them (io.py:160-172), byte for byte.
 """
 
 from __future__ import annotations
@@ -247,7 +250,30 @@ def genotypes():
     (OUT / "genotype.json").write_text(json.dumps(rows, indent=1) + "\n")
 
 
+def fidm_cases():
+    from fastid import io as ref_io
+
+    rng = np.random.default_rng(0xF1D)
+    cases = {}
+    r4 = np.array([[0xF0000000], [0x0F000000], [0xFF000000], [0x00000000]], np.uint32)
+    q4 = np.array([[0xF0000000], [0x0F000000], [0xA0000000], [0xCC000000]], np.uint32)
+    r_rand, _ = rand_words(rng, 37, 2, 64, 100)
+    q_rand, _ = rand_words(rng, 23, 2, 64, 100)
+    for name, r, q, L in (("golden_4x4", r4, q4, 8), ("rand_37x23_L100", r_rand, q_rand, 100)):
+        m = kernel.compare_naive(panel(r, L, "r"), panel(q, L, "q"))
+        with tempfile.TemporaryDirectory() as d:
+            path = Path(d) / "scores.fidm"
+            ref_io.write_scores(m, ref_io.ScoreOutput(path=str(path), format="binary"))
+            blob = np.frombuffer(path.read_bytes(), np.uint8)
+        cases[f"{name}__refs"] = r
+        cases[f"{name}__queries"] = q
+        cases[f"{name}__bits"] = np.array(L)
+        cases[f"{name}__fidm"] = blob
+    np.savez_compressed(OUT / "fidm_cases.npz", **cases)
+
+
 if __name__ == "__main__":
+    fidm_cases()
     kernel_cases()
     topk_cases()
     pack_cases()

@@ -178,6 +178,26 @@ def test_compare_b200_large_result(rng):
     assert np.array_equal(got.scores, oracle.naive(r, q))
 
 
+def test_compare_to_fidm_matches_reference_files(tmp_path, rng):
+    """compare_to_fidm writes the reference's packed-binary score file byte for
+    byte (reference-written goldens), small and through several pipeline chunks."""
+    m = fb()
+    d = np.load(GOLDEN / "fidm_cases.npz")
+    for name in ("golden_4x4", "rand_37x23_L100"):
+        r, q, L = d[f"{name}__refs"], d[f"{name}__queries"], int(d[f"{name}__bits"])
+        path = tmp_path / f"{name}.fidm"
+        m.compare_to_fidm(m.Panel(tuple(range(len(r))), r, L), m.Panel(tuple(range(len(q))), q, L), path)
+        assert path.read_bytes() == d[f"{name}__fidm"].tobytes(), name
+    n_r, n_q, L = 70_000, 300, 256
+    r, _ = rand_words(rng, n_r, L // 64, 64, L)
+    q, _ = rand_words(rng, n_q, L // 64, 64, L)
+    path = tmp_path / "big.fidm"
+    assert m.compare_to_fidm(m.Panel(tuple(range(n_r)), r, L), m.Panel(tuple(range(n_q)), q, L), path) == (n_r, n_q)
+    blob = path.read_bytes()
+    assert blob[:21] == __import__("struct").pack("<4sBQQ", b"FIDM", 1, n_r, n_q)
+    assert np.array_equal(np.frombuffer(blob[21:], "<u4").reshape(n_r, n_q), oracle.naive(r, q))
+
+
 def test_executor_seam(rng):
     m = fb()
     r, _ = rand_words(rng, 100, 4, 64)

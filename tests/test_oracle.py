@@ -96,3 +96,22 @@ def test_c_and_numpy_agree_random(rng, width):
         r, _ = rand_words(rng, 40, nw, width, L)
         q, _ = rand_words(rng, 23, nw, width, L)
         assert np.array_equal(oracle.naive(r, q), oracle.np_scores(r, q))
+
+
+def fidm_bytes(scores: np.ndarray) -> bytes:
+    """The packed-binary score file (io.py:29-31 header, then row-major <u4 cells), restated."""
+    import struct
+
+    n_r, n_q = scores.shape
+    return struct.pack("<4sBQQ", b"FIDM", 1, n_r, n_q) + np.ascontiguousarray(scores, "<u4").tobytes()
+
+
+def test_fidm_format_matches_reference_files():
+    """The oracle's scores in the FIDM layout equal the files the reference's own
+    write_scores produced (tests/golden/fidm_cases.npz)."""
+    from conftest import GOLDEN
+
+    d = np.load(GOLDEN / "fidm_cases.npz")
+    for name in ("golden_4x4", "rand_37x23_L100"):
+        r, q = d[f"{name}__refs"], d[f"{name}__queries"]
+        assert fidm_bytes(oracle.naive(r, q)) == d[f"{name}__fidm"].tobytes(), name

@@ -29,3 +29,18 @@ pick = rng.integers(0, n_r, 32)
 ok = np.array_equal(out[pick], oracle.naive(r[pick], q))
 print(f"run_b200_kernel {n_r}x{n_q}x{L}: {t*1e3:.1f} ms  ({n_r*n_q*4/t/1e9:.1f} GB/s of u32 output, "
       f"{n_r*n_q/t:.3e} cmp/s)  oracle rows ok={ok}", flush=True)
+
+# the same matrix streamed into a packed-binary (FIDM) score file
+import os, tempfile
+R = m.Panel(tuple(range(n_r)), r, L)
+Q = m.Panel(tuple(range(n_q)), q, L)
+with tempfile.TemporaryDirectory(dir=os.environ.get("FASTID_FIDM_DIR")) as d:
+    path = os.path.join(d, "scores.fidm")
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        m.compare_to_fidm(R, Q, path)
+        ts.append(time.perf_counter() - t0)
+        os.unlink(path)
+    t = min(ts)
+    print(f"compare_to_fidm {n_r}x{n_q}x{L}: {t*1e3:.1f} ms  ({n_r*n_q*4/t/1e9:.1f} GB/s into {d})", flush=True)
