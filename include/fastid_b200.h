@@ -51,7 +51,9 @@ enum fastid_status {
     FASTID_E_CUDA = 3,        /* CUDA runtime/driver failure                      */
     FASTID_E_CAPACITY = 4,    /* output buffer too small; count still reported    */
     FASTID_E_NOMEM = 5,       /* device allocation failed                         */
-    FASTID_E_UNSUPPORTED = 6  /* formulation/shape not supported on this device   */
+    FASTID_E_UNSUPPORTED = 6, /* formulation/shape not supported on this device   */
+    FASTID_E_FORMAT = 7,      /* malformed panel text (maps to PanelFormatError)  */
+    FASTID_E_CORRUPT = 8      /* nonzero padding (maps to CorruptProfileError)    */
 };
 
 enum fastid_formulation {
@@ -203,6 +205,25 @@ FASTID_API int fastid_probe_tmem_read(int x, int warps, int iters, void* scratch
 FASTID_API int fastid_probe_contention(int iters, int readers, void* sink, void* stream);
 FASTID_API int fastid_probe_variant(int formulation, int variant, int iters, void* scratch, const void* src,
                                     int64_t src_bytes, double* work, void* stream);
+
+/* ---- bulk panel ingest (host) ------------------------------------------- */
+
+/* Parse the reference's text panel format (io.load_panel, io.py:45-127):
+ * `#bits=<L>` header, `#` comments, blank lines, `<id><TAB><hex>` profiles,
+ * universal newlines.  Same validation order and messages as the reference
+ * (FASTID_E_FORMAT -> PanelFormatError, FASTID_E_CORRUPT -> CorruptProfileError,
+ * first offending line wins).  Words are word_width (32|64) bits, native
+ * endian, row-major n x ceil(L/W).  n_threads <= 0: all hardware threads. */
+typedef struct fastid_parsed_panel fastid_parsed_panel;
+FASTID_API int fastid_parse_panel(const char* text, int64_t len, int word_width, int n_threads,
+                                  fastid_parsed_panel** out);
+FASTID_API int fastid_parsed_panel_shape(const fastid_parsed_panel* p, int64_t* n_profiles, int64_t* bit_length,
+                                         int64_t* n_words, int64_t* id_bytes);
+/* words: n x n_words words; ids: id_bytes bytes (UTF-8, the ids joined by
+ * '\n'); id_offsets: n + 1 byte offsets of each id in ids (last = id_bytes).
+ * Any pointer may be NULL. */
+FASTID_API int fastid_parsed_panel_copy(const fastid_parsed_panel* p, void* words, char* ids, int64_t* id_offsets);
+FASTID_API void fastid_parsed_panel_free(fastid_parsed_panel* p);
 
 #ifdef __cplusplus
 }

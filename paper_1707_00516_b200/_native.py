@@ -15,14 +15,14 @@ import subprocess
 import threading
 from pathlib import Path
 
-from .errors import CapacityError, DeviceError, PanelMismatchError
+from .errors import CapacityError, CorruptProfileError, DeviceError, PanelFormatError, PanelMismatchError
 
 PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 INCLUDE = REPO_DIR / "include"
 LIB_PATH = PKG_DIR / "_fastid_b200.so"
-SOURCES = ("api.cu", "encode.cu", "popc.cu", "tensor.cu", "merge.cu", "probe.cu")
+SOURCES = ("api.cu", "encode.cu", "popc.cu", "tensor.cu", "merge.cu", "probe.cu", "ingest.cu")
 HEADERS = ("common.cuh", "tensor_ptx.cuh")
 
 NVCC_FLAGS = (
@@ -32,7 +32,7 @@ NVCC_FLAGS = (
     "--expt-relaxed-constexpr",
 )
 
-FASTID_OK, E_INVALID, E_MISMATCH, E_CUDA, E_CAPACITY, E_NOMEM, E_UNSUPPORTED = range(7)
+FASTID_OK, E_INVALID, E_MISMATCH, E_CUDA, E_CAPACITY, E_NOMEM, E_UNSUPPORTED, E_FORMAT, E_CORRUPT = range(9)
 FORMULATIONS = {"auto": 0, "popc": 1, "tensor_i8": 2, "tensor_f4": 3}
 
 _lock = threading.Lock()
@@ -101,6 +101,11 @@ def lib() -> ctypes.CDLL:
             "fastid_merge_topk": ([vp, vp, i32, i64, i32, i32, vp, vp, vp], i32),
             "fastid_run_kernel": ([vp, i64, vp, i64, i64, i32, i32, vp, i32], i32),
             "fastid_run_kernel_fd": ([vp, i64, vp, i64, i64, i32, i32, i32, i32], i32),
+            "fastid_parse_panel": ([vp, i64, i32, i32, ctypes.POINTER(vp)], i32),
+            "fastid_parsed_panel_shape": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                           ctypes.POINTER(i64)], i32),
+            "fastid_parsed_panel_copy": ([vp, vp, vp, vp], i32),
+            "fastid_parsed_panel_free": ([vp], None),
             "fastid_db_image_bytes": ([i64, i64, i32], sz),
             "fastid_db_create": ([vp, i64, i64, i64, i32, vp, ctypes.POINTER(vp)], i32),
             "fastid_db_destroy": ([vp], i32),
@@ -145,6 +150,10 @@ def check(status: int, what: str) -> None:
         raise PanelMismatchError(msg)
     if status == E_CAPACITY:
         raise CapacityError(msg, required=-1)
+    if status == E_FORMAT:
+        raise PanelFormatError(msg)
+    if status == E_CORRUPT:
+        raise CorruptProfileError(msg)
     raise DeviceError(msg)
 
 

@@ -21,6 +21,10 @@ reference tree) and records, for a set of seeded inputs:
                        ``compare_blocked`` on ``synth_panel`` inputs
                        (bench.py:41-54), incl. BASELINE config 1;
 * genotype.json     -- ``codec.encode_genotype`` examples (codec.py:99-115);
+* panel_cases.json  -- panel texts (valid and malformed) and what the
+                       reference's ``io.load_panel`` returns for them at word
+                       widths 32 and 64: ids, bit length, hex words -- or the
+                       exception type and message (io.py:45-127);
 * fidm_cases.npz    -- panels and the packed-binary score files the reference's
                        own ``io.write_scores(..., ScoreOutput(path, "binary"))``
                        writes for them (io.py:160-172), byte for byte.
@@ -272,7 +276,80 @@ def fidm_cases():
     np.savez_compressed(OUT / "fidm_cases.npz", **cases)
 
 
+def panel_texts():
+    rng = np.random.default_rng(0x1A57)
+    texts = {
+        "worked_example": "#bits=32\nS1\t06001440\n",
+        "empty_body": "#bits=64\n",
+        "ids_in_order": "#bits=8\nba\t00\nc\tFF\nab\t0F\n",
+        "comments": "# comment\n#bits=8\n# another\nx\tA5\n",
+        "missing_header": "S1\t06001440\n",
+        "before_header": "S1\t00\n#bits=8\n",
+        "duplicate_id": "#bits=8\na\t00\na\tFF\n",
+        "length_mismatch": "#bits=8\na\t00\nb\t0000\n",
+        "tail_padding": "#bits=4\na\t01\n",
+        "surplus_padding": "#bits=32\na\t0600144000000001\n",
+        "comma_id": "#bits=8\na,b\t00\n",
+        "bad_hex": "#bits=8\na\tZZ\n",
+        "bad_hex_mixed": "#bits=8\na\t0q\nb\tz!\n",
+        "short_hex": "#bits=64\na\t00\n",
+        "duplicate_header": "#bits=8\n#bits=8\na\t00\n",
+        "duplicate_header_after_profile": "#bits=8\na\t00\n#bits=16\n",
+        "bad_header": "#bits=abc\n",
+        "zero_bits": "#bits=0\n",
+        "negative_bits": "#bits=-3\n",
+        "header_spaces_underscore": "#  bits= 1_6 \na\tFFFF\n",
+        "three_fields": "#bits=8\na\t00\tff\n",
+        "no_tab": "#bits=8\na 00\n",
+        "empty_id": "#bits=8\n\t00\n",
+        "empty_hex_short": "#bits=8\na\t\n",
+        "crlf_and_cr": "#bits=12\r\na\tABC\r\nb\t123\rc\tfff\n\n\r\n",
+        "lowercase_zero_extend_truncate": "#bits=40\np1\tdeadbeef12\np2\t0000000000\n",
+        "truncate_zero_surplus": "#bits=8\np\tA500000000000000000000\n",
+        "dup_vs_bad_hex_same_line": "#bits=8\na\t00\na\tZZ\n",
+        "error_order_first_line_wins": "#bits=8\na\t00\nb\tZZ\nb\t00\n",
+        "missing_header_no_profiles": "# only a comment\n\n",
+        "unicode_id": "#bits=8\n\u00e9t\u00e9\t7F\n",
+    }
+    for L in (1, 50, 64, 100, 1000):
+        n_digits = -(-L // 4)
+        lines = [f"#bits={L}", "# generated"]
+        for i in range(60):
+            bits = rng.integers(0, 2, L)
+            val = int("".join(map(str, bits)), 2) << (4 * n_digits - L) if L else 0
+            h = f"{val:0{n_digits}x}" if i % 2 else f"{val:0{n_digits}X}"
+            h = h + "0" * (L % 3 + (L == 64))  # surplus zero digits (same on every line): truncated
+            lines.append(f"id{i}_{L}\t{h}")
+            if i % 11 == 5:
+                lines.append("")
+        texts[f"random_L{L}"] = "\n".join(lines) + "\n"
+    return texts
+
+
+def panel_cases():
+    from fastid import errors as ref_errors
+    from fastid import io as ref_io
+
+    out = []
+    for name, text in panel_texts().items():
+        row = {"name": name, "text": text, "results": {}}
+        for width in (32, 64):
+            with tempfile.TemporaryDirectory() as d:
+                path = Path(d) / "p.panel"
+                path.write_bytes(text.encode("utf-8"))
+                try:
+                    p = ref_io.load_panel(path, width)
+                    row["results"][str(width)] = {"ids": list(p.ids), "bit_length": p.bit_length,
+                                                  "words": [[f"{int(w):x}" for w in r] for r in p.words]}
+                except (ref_errors.PanelFormatError, ref_errors.CorruptProfileError) as e:
+                    msg = str(e).replace(str(path), "<path>")
+                    row["results"][str(width)] = {"error": type(e).__name__, "message": msg}
+        out.append(row)
+    (OUT / "panel_cases.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
 if __name__ == "__main__":
+    panel_cases()
     fidm_cases()
     kernel_cases()
     topk_cases()
