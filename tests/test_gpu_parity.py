@@ -368,3 +368,26 @@ def test_pairs_more_groups_than_sms(rng):
     assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex)
     full = db.full_device(m.DevicePanel.from_words(q[:300], L)).cpu().numpy().view(np.uint32)
     assert np.array_equal(full, oracle.naive(r, q[:300]))
+
+
+def test_cli_compare_and_search(tmp_path):
+    """python -m paper_1707_00516_b200 compare / search on panel files: the
+    binary output is the reference-written FIDM file, the CSV the reference's
+    golden scores_4x4.csv bytes, search the oracle's top-k."""
+    m = fb()
+    from paper_1707_00516_b200.__main__ import main
+    from paper_1707_00516_b200.ingest import save_panel
+
+    d = np.load(GOLDEN / "fidm_cases.npz")
+    r, q = d["golden_4x4__refs"], d["golden_4x4__queries"]
+    save_panel(m.Panel(tuple(f"r{i}" for i in range(4)), r, 8), tmp_path / "r.panel")
+    save_panel(m.Panel(tuple(f"q{j}" for j in range(4)), q, 8), tmp_path / "q.panel")
+    args = ["--refs", str(tmp_path / "r.panel"), "--queries", str(tmp_path / "q.panel"), "--word-width", "32"]
+    assert main(["compare", *args, "--out", str(tmp_path / "s.fidm"), "--format", "binary"]) == 0
+    assert (tmp_path / "s.fidm").read_bytes() == d["golden_4x4__fidm"].tobytes()
+    assert main(["compare", *args, "--out", str(tmp_path / "s.csv")]) == 0
+    assert (tmp_path / "s.csv").read_text() == "ref_id,q0,q1,q2,q3\nr0,0,4,2,2\nr1,4,0,4,2\nr2,4,4,6,4\nr3,0,0,0,0\n"
+    assert main(["search", *args, "--out", str(tmp_path / "t.csv"), "-k", "2"]) == 0
+    rows = (tmp_path / "t.csv").read_text().splitlines()
+    assert rows[0] == "query_id,rank,ref_id,score" and rows[1:3] == ["q0,1,r0,0", "q0,2,r3,0"]
+    assert main(["compare", "--refs", str(tmp_path / "missing"), "--queries", "x", "--out", "y"]) == 1

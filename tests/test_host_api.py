@@ -91,3 +91,14 @@ def test_mismatch_checked_before_device():
     # empty panels need no device
     e = fb.Panel((), np.zeros((0, 2), np.uint32), 64)
     assert fb.compare_b200(e, a).shape == (0, 1)
+
+
+def test_cli_exit_codes(tmp_path):
+    """Usage errors exit 2 (argparse), unreadable inputs exit 1 -- cli.py:3-4, 231-241."""
+    import pytest
+    from paper_1707_00516_b200.__main__ import main
+
+    with pytest.raises(SystemExit) as info:
+        main(["compare", "--refs", "a"])
+    assert info.value.code == 2
+    assert main(["compare", "--refs", str(tmp_path / "nope"), "--queries", "q", "--out", "o"]) == 1
