@@ -68,6 +68,7 @@ struct Roles {
 // the others, so an epilogue warp that runs late on one tile (top-k
 // insertions) does not stall the tensor pipe.
 constexpr int kAccBufs = 2;
+
 constexpr int kDriftTiles = 40;  // max lead of a pair over the slowest pair of its slice
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
 constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
@@ -111,6 +112,17 @@ __device__ __forceinline__ uint4 unpack_f4(uint32_t w) {
     }
     return make_uint4((w << 2) & 0x44444444u, w & 0x22222222u, (w >> 2) & 0x11111111u, (w >> 3) & 0x11111111u);
 }
+// The prepared image and the A operands matched with it use one value for
+// every set bit (e2m1 0x2 = 1.0 on both sides, product 1.0): the shifts cost
+// nothing there (built once).  Kernel time is the same as with the weighted
+// pairs above (tools/encoding_ab.py: 11.42 vs 11.41 ms on C3).
+__device__ __forceinline__ uint4 unpack_f4_uniform(uint32_t w) {
+    return make_uint4((w & 0x11111111u) << 1, w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
+}
+// debug flag 512 keeps the weighted encoding for the image too (A/B timing; image and
+// queries must be prepared under the same setting)
+__device__ __forceinline__ bool uniform_image(const CompareArgs& a) { return !(a.debug_flags & 512); }
+
 template <bool B_SIDE>
 __device__ __forceinline__ void unpack_i8(uint32_t w, uint4& lo, uint4& hi) {
     if (B_SIDE) {
@@ -576,7 +588,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     for (int i = 0; i < 4; ++i) {
                         const int col = (w4 + i) * CPW;
                         if (F == FASTID_TENSOR_F4) {
-                            *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) = unpack_f4<false>(wv[i]);
+                            *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) =
+                                IMG && uniform_image(a) ? unpack_f4_uniform(wv[i]) : unpack_f4<false>(wv[i]);
                         } else {
                             uint4 lo, hi;
                             unpack_i8<false>(wv[i], lo, hi);
@@ -1023,7 +1036,8 @@ __global__ void prep_a_kernel(CompareArgs a, int n_groups, int n_kst, uint8_t* _
             uint32_t x = 0;
             if (real && word < row_words) x = ~reinterpret_cast<const uint32_t*>(a.queries + q * a.stride)[word];
             if (F == FASTID_TENSOR_F4) {
-                *reinterpret_cast<uint4*>(dst + core_off(row, w, kM)) = unpack_f4<false>(x);
+                *reinterpret_cast<uint4*>(dst + core_off(row, w, kM)) =
+                    a.image && uniform_image(a) ? unpack_f4_uniform(x) : unpack_f4<false>(x);
             } else {
                 uint4 lo, hi;
                 unpack_i8<false>(x, lo, hi);
@@ -1234,7 +1248,7 @@ __global__ void build_image_kernel(CompareArgs a, int64_t n_tiles, int n_kst, ui
         for (int i = 0; i < 4; ++i) {
             if (F == FASTID_TENSOR_F4) {
                 *reinterpret_cast<uint4*>(dst + hr * (UB / 2) + core_off(row - hr * (BN / 2), col0 + i, BN / 2)) =
-                    unpack_f4<true>(wv[i]);
+                    uniform_image(a) ? unpack_f4_uniform(wv[i]) : unpack_f4<true>(wv[i]);
             } else {
                 uint4 lo, hi;
                 unpack_i8<true>(wv[i], lo, hi);
