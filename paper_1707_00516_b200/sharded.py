@@ -41,7 +41,7 @@ def gather_candidates(scores: torch.Tensor, index: torch.Tensor, group=None):
     world = dist.get_world_size(group)
     s_all = torch.empty((world, *scores.shape), dtype=scores.dtype, device=scores.device)
     x_all = torch.empty((world, *index.shape), dtype=index.dtype, device=index.device)
-    if hasattr(dist, "all_gather_into_tensor") and scores.is_cuda:
+    if scores.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(s_all, scores.contiguous(), group=group)
         dist.all_gather_into_tensor(x_all, index.contiguous(), group=group)
     else:
