@@ -8,22 +8,23 @@
 // values in {0, 1} with unit (ue8m0 = 127) block scales and accumulates
 // integers <= L in fp32.
 //
-// One CTA per SM (persistent), warp-specialised:
-//   warp 0      TMA producer: 2-D tensor copies of packed known rows
-//               (BN rows x 32 B = 256 loci per stage) into a deep ring.
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma into a
-//               triple-buffered TMEM accumulator (BN fp32/s32 columns each).
-//   warps 2-5   converters: unpack the packed bits into the UMMA K-major
-//               operand layout (e2m1 nibbles or int8 bytes); at start-up they
-//               also build the resident A operand = complemented unknown tile.
-//   warps 6-9   epilogue: tcgen05.ld the accumulator (one TMEM lane = one
-//               unknown per thread) and apply the fused epilogue: full u32
-//               store, per-unknown top-k, or threshold hits.
-// The unknown tile (128 unknowns) stays resident in shared memory for the
-// CTA's whole slice of known tiles; known tiles stream through TMA.  CTAs of
-// the same slice index walk the same known tiles at the same time, so each
-// known tile is read from HBM once and served to the other unknown groups
-// from L2.  DESIGN.md has the roofline and byte accounting.
+// Persistent, warp-specialised kernels (one CTA per SM; roles in Roles<>):
+//   * packed operands: 8 converter warps unpack the TMA-streamed packed known
+//     rows into the UMMA K-major operand layout every tile, 8 epilogue warps;
+//   * prepared image (KnownDatabase): the operand bytes stream straight into
+//     the ring, 12 (mxf4) / 16 (i8) epilogue warps; for mxf4 a CTA pair
+//     (cluster of 2, tcgen05.mma.cta_group::2, M = 256) shares every known
+//     tile, each CTA streaming half of it;
+//   * one producer warp (TMA / bulk copies) and one MMA warp; each keeps the
+//     whole warp in its loop and elects one lane to issue.
+// The MMA fills one of two TMEM accumulators (BN fp32/s32 columns) while the
+// epilogue drains the other: full u32 store (TMA tensor stores for pairs),
+// per-unknown top-k with a shared admission bound, or threshold hits.
+// The unknown tile (128 unknowns per CTA) stays resident in shared memory
+// (streamed per stage for long profiles).  CTAs of one slice index walk the
+// same known tiles at the same time, with bounded drift, so each known tile
+// is read from HBM once and served to the other unknown groups from L2.
+// DESIGN.md has the roofline and byte accounting.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
