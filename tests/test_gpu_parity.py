@@ -391,3 +391,45 @@ def test_cli_compare_and_search(tmp_path):
     rows = (tmp_path / "t.csv").read_text().splitlines()
     assert rows[0] == "query_id,rank,ref_id,score" and rows[1:3] == ["q0,1,r0,0", "q0,2,r3,0"]
     assert main(["compare", "--refs", str(tmp_path / "missing"), "--queries", "x", "--out", "y"]) == 1
+
+
+@pytest.mark.parametrize("shape", [(60_000, 2048, 1024), (80_000, 700, 512), (40_000, 1024, 2304)])
+def test_pairs_with_spare_pairs(rng, shape):
+    """Enough known tiles that the SMs left over by (unknown groups x slices) run
+    spare CTA pairs over the tail tiles of several groups in turn (rebuilding the
+    resident or streamed unknowns between groups): top-k, threshold and full
+    rows equal the oracle, and equal the launch without spares (debug flag 1024)."""
+    import torch
+
+    m = fb()
+    from paper_1707_00516_b200 import _native
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    n_r, n_q, L = shape
+    nw = L // 64
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    q, _ = rand_words(rng, n_q, nw, 64, L)
+    q[::5] = r[rng.integers(n_r - n_r // 30, n_r, len(q[::5]))]  # near the tail the spares own
+    db = KnownDatabase(r, L, formulation="tensor_f4")
+    s, x = db.search_words(q, 16)
+    pick = np.arange(0, n_q, 7)
+    es, ex, _ = oracle.topk(r, q[pick], 16)
+    assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex)
+    lib = _native.lib()
+    lib.fastid_debug_flags(1024)
+    try:
+        s2, x2 = db.search_words(q, 16)
+    finally:
+        lib.fastid_debug_flags(0)
+    assert np.array_equal(s, s2) and np.array_equal(x, x2)
+    dq = m.DevicePanel.from_words(q, L)
+    full = db.full_device(dq)
+    rows = np.concatenate([np.arange(0, 64), np.arange(n_r - 300, n_r)])
+    got = full[torch.from_numpy(rows).cuda()].cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, oracle.naive(r[rows], q))
+    thr = L // 8  # planted copies (0) only; random pairs sit near L/4
+    hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
+    sub = oracle.naive(r[n_r - 300:], q)
+    hq, hr, hs = oracle.threshold_from_matrix(sub, thr)
+    sel = hits.ref >= n_r - 300
+    assert np.array_equal(hits.query[sel], hq) and np.array_equal(hits.ref[sel], hr + n_r - 300)
