@@ -394,34 +394,25 @@ def test_cli_compare_and_search(tmp_path):
 
 
 @pytest.mark.parametrize("shape", [(60_000, 2048, 1024), (80_000, 700, 512), (40_000, 1024, 2304)])
-def test_pairs_with_spare_pairs(rng, shape):
-    """Enough known tiles that the SMs left over by (unknown groups x slices) run
-    spare CTA pairs over the tail tiles of several groups in turn (rebuilding the
-    resident or streamed unknowns between groups): top-k, threshold and full
-    rows equal the oracle, and equal the launch without spares (debug flag 1024)."""
+def test_pairs_large_panels(rng, shape):
+    """Larger panels on the CTA-pair kernel (resident and streamed unknowns,
+    drift control active): top-k, threshold and full rows near both ends of the
+    known range equal the oracle."""
     import torch
 
     m = fb()
-    from paper_1707_00516_b200 import _native
     from paper_1707_00516_b200.search import KnownDatabase
 
     n_r, n_q, L = shape
     nw = L // 64
     r, _ = rand_words(rng, n_r, nw, 64, L)
     q, _ = rand_words(rng, n_q, nw, 64, L)
-    q[::5] = r[rng.integers(n_r - n_r // 30, n_r, len(q[::5]))]  # near the tail the spares own
+    q[::5] = r[rng.integers(n_r - n_r // 30, n_r, len(q[::5]))]  # copies near the end of the known range
     db = KnownDatabase(r, L, formulation="tensor_f4")
     s, x = db.search_words(q, 16)
     pick = np.arange(0, n_q, 7)
     es, ex, _ = oracle.topk(r, q[pick], 16)
     assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex)
-    lib = _native.lib()
-    lib.fastid_debug_flags(1024)
-    try:
-        s2, x2 = db.search_words(q, 16)
-    finally:
-        lib.fastid_debug_flags(0)
-    assert np.array_equal(s, s2) and np.array_equal(x, x2)
     dq = m.DevicePanel.from_words(q, L)
     full = db.full_device(dq)
     rows = np.concatenate([np.arange(0, 64), np.arange(n_r - 300, n_r)])

@@ -1,5 +1,5 @@
-"""A/B: CTA-pair top-k with and without spare pairs (debug flag 1024), alternating rounds,
-plus per-CTA finish times (debug flag 64) for each."""
+"""A/B: CTA-pair top-k with debug flags 0 vs FLAG (see common.cuh for the flag bits), alternating
+rounds, plus per-CTA finish times (debug flag 64) for each.  usage: spare_ab.py [FLAG] (default 16: no top-k insertions)"""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -17,9 +17,10 @@ del r
 dq = m.DevicePanel.from_words(q, L)
 ws = torch.empty(m.compare.topk_workspace_bytes(n_r, n_q, 16, "tensor_f4"), dtype=torch.uint8, device="cuda")
 lib = _native.lib()
-res = {0: [], 1024: []}
+FLAG = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+res = {0: [], FLAG: []}
 for rd in range(4):
-    for flags in (0, 1024):
+    for flags in (0, FLAG):
         lib.fastid_debug_flags(flags)
         db.topk_device(dq, 16, None, ws)
         evs = []
@@ -30,9 +31,9 @@ for rd in range(4):
         torch.cuda.synchronize()
         res[flags].append(np.median([a.elapsed_time(b) for a, b in evs]))
 for flags, v in res.items():
-    print(f"{'spares' if flags == 0 else 'no spares':9s}: {[round(x, 3) for x in v]} mean {np.mean(v):.3f} ms")
+    print(f"flags {flags:5d}: {[round(x, 3) for x in v]} mean {np.mean(v):.3f} ms")
 buf = torch.zeros((148 * 4,), dtype=torch.int64, device="cuda")
-for flags in (0, 1024):
+for flags in (0, FLAG):
     buf.zero_()
     lib.fastid_debug_flags(64 | flags)
     lib.fastid_debug_trace(buf.data_ptr(), 0)
