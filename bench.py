@@ -450,7 +450,10 @@ def run_b200(args):
         "kernel_ms": kern_avg * 1e3,
         "kernel_share_of_step": kern_avg / (elapsed / args.steps),
         "algorithmic": f"{macs:.4g} bit-pair MACs per launch = {n_local} knowns x {args.n_unknown} unknowns x {L} loci",
-        "hbm_gbs": (n_local * db.panel.stride) / kern_avg / 1e9,
+        # bytes the kernel must read from HBM per launch (the mxf4 tensor image for the
+        # tensor path, the packed rows otherwise) over its time: far below the HBM roof
+        "hbm_gbs": ((n_local * ((L + 255) // 256) * 256 // 2 if formulation == "tensor_f4"
+                     else n_local * db.panel.stride) + args.n_unknown * db.panel.stride) / kern_avg / 1e9,
         "hbm_peak_gbs": peaks.get("hbm_gbs"),
         "bf16_tflops_measured": peaks.get("bf16_tflops"),
     }
