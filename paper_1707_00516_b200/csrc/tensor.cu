@@ -256,10 +256,22 @@ struct Layout {
             a_bytes = n_kst * kAStageBytes;
             place();
         } else {
-            for (sa = kMaxAStages; sa >= 2; --sa) {
+            // deepest A ring that still leaves an operand ring of >= 4 stages,
+            // else >= 3, else >= 2 (A and B stages are consumed in lockstep)
+            bool ok = false;
+            for (int min_su = 4; min_su >= 2 && !ok; --min_su)
+                for (sa = kMaxAStages; sa >= 2; --sa) {
+                    a_bytes = sa * kAStageBytes;
+                    place();
+                    if (fits() && su >= min_su) {
+                        ok = true;
+                        break;
+                    }
+                }
+            if (!ok) {  // nothing fits: leave an unfit layout for the caller to reject
+                sa = 2;
                 a_bytes = sa * kAStageBytes;
                 place();
-                if (fits()) break;
             }
         }
     }
