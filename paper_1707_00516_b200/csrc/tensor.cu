@@ -312,7 +312,7 @@ constexpr int out_stage_bytes() {
 // the known tile (BN/2 rows of the prepared image) -- half the L2->SM operand
 // traffic per MAC of the single-CTA kernel, which is L2-throughput-bound.
 // The leader (rank 0) issues every MMA; the commits multicast to both CTAs.
-template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
+template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR, bool SPARE>
 __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     tensor_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                   const __grid_constant__ CUtensorMap amap, CompareArgs a, const uint8_t* __restrict__ a_global,
@@ -359,11 +359,23 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // CTA pair or CTA
-    const int group = unit / n_slices;
-    const int slice = unit - group * n_slices;
-    const int64_t q0 = ((int64_t)group * (PAIR ? 2 : 1) + rank) * kM;
-    const int64_t t_begin = n_tiles * slice / n_slices;
-    const int64_t t_end = n_tiles * (slice + 1) / n_slices;
+    // Work segments.  A regular unit owns slice `unit % n_slices` of the first
+    // t_main tiles for unknown group `unit / n_slices`.  Spare CTA pairs (the
+    // SMs left over by groups x slices, a.n_spare of them) each take the last
+    // n_tiles - t_main tiles of a_groups / n_spare groups in turn, as list
+    // slot n_slices, rebuilding the resident unknowns between groups.
+    // (the spare pairs are a separate launch, SPARE = true, on the SMs the
+    // regular grid leaves free; for regular launches every loop over
+    // segments has a compile-time trip count of 1)
+    constexpr bool spare = SPARE;
+    const int per_spare = SPARE ? a.n_groups / a.n_spare : 1;
+    const int n_seg = SPARE ? per_spare : 1;
+    const int64_t t_main = PAIR && a.n_spare ? a.t_main : n_tiles;
+    const int slice = spare ? n_slices : unit % n_slices;  // partial-list slot
+    const int64_t t_begin = spare ? t_main : t_main * slice / n_slices;
+    const int64_t t_end = spare ? n_tiles : t_main * (slice + 1) / n_slices;
+    auto seg_group = [&](int sg) { return spare ? unit * per_spare + sg : unit / n_slices; };
+    auto seg_q0 = [&](int sg) { return ((int64_t)seg_group(sg) * (PAIR ? 2 : 1) + rank) * kM; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < SP; ++i) {
@@ -421,11 +433,15 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             // HBM once and served to the other groups from L2: the leader's
             // producer publishes its progress and waits (bounded) while it leads
             // the slowest pair of its slice by more than that.
-            int* prog = (PAIR && leader && a.progress) ? a.progress + (int64_t)slice * a.n_groups : nullptr;
+            int* prog = (PAIR && leader && a.progress && !spare) ? a.progress + (int64_t)slice * a.n_groups : nullptr;
+            const int group = seg_group(0);  // drift control: regular units only (one segment)
             // The peers' counters are loaded at one check and consumed at the next,
             // so their latency never stalls the operand stream.
             int local_t = 0;
             int peer = 0x7FFFFFFF;  // this lane's peer counter, in flight since the last check
+            for (int sg = 0; sg < n_seg; ++sg) {
+            // first 128-B row of this segment's streamed-A stages (warp-uniform, hoisted)
+            const int64_t a_row0 = ((int64_t)seg_group(sg) * 2 + rank) * n_kst * (AB / 128);
             for (int64_t t = t_begin; t < t_end; ++t, ++local_t) {
                 if (prog && (local_t & 7) == 0) {
                     int lo = __reduce_min_sync(0xFFFFFFFFu, peer);
@@ -452,7 +468,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                                 // barrier counts both
                                 if (leader) ptx::mbar_expect_tx(&ar_full[sa], 2 * AB);
                                 ptx::tma_load_2d_pair(sA + sa * AB, &amap, ptx::mapa(&ar_full[sa], 0), 0,
-                                                      (int)((((int64_t)group * 2 + rank) * n_kst + ks) * (AB / 128)));
+                                                      (int)(a_row0 + (int64_t)ks * (AB / 128)));
                             } else {
                                 ptx::mbar_expect_tx(&ar_full[sa], AB);
                                 ptx::bulk_load(sA + sa * AB, a_global + ((int64_t)group * n_kst + ks) * AB, AB,
@@ -500,7 +516,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     __syncwarp();
                 }
             }
-            if (PAIR && leader && a.progress && lane == 0)
+            }
+            if (PAIR && leader && a.progress && !spare && lane == 0)
                 ptx::st_relaxed(a.progress + (int64_t)slice * a.n_groups + group, 0x7FFFFFFF);  // finished: never waited on
         }
     } else if (warp == kMmaWarp) {
@@ -513,15 +530,16 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             constexpr int kBRows = kSplitB ? BN / 2 : BN;  // rows per B core-matrix column
             const uint64_t a_desc0 = ptx::smem_desc(ptx::smem_u32(sA), kM * 16, 128);
             const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(sU), kBRows * 16, 128);
-            if (!SA) {
-                if (PAIR)
-                    ptx::mbar_wait_cluster(a_full, 0);
-                else
-                    ptx::mbar_wait(a_full, 0);
-            }
-            ptx::tc_fence_after();
             Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
+            for (int sg = 0; sg < n_seg; ++sg) {
+            if (!SA) {  // this segment's resident unknowns are built (phase sg of a_full)
+                if (PAIR)
+                    ptx::mbar_wait_cluster(a_full, (uint32_t)sg & 1u);
+                else
+                    ptx::mbar_wait(a_full, (uint32_t)sg & 1u);
+            }
+            ptx::tc_fence_after();
             for (int64_t t = t_begin; t < t_end; ++t, ++local) {
                 const int acc = local % kAccBufs;
                 const uint32_t use = (uint32_t)(local / kAccBufs) & 1u;  // parity of this buffer's use
@@ -579,14 +597,17 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 __syncwarp();
                 if (tr) a.trace[local * kTrSlots + kTrMmaIssued] = clock64();
             }
+            }
         }
     } else {
         const int ct = threadIdx.x;  // 0..kConvThreads-1 for converters
-        if (warp < kBuildWarps) {
+        // Resident A = complemented unknown rows of one segment's group; zero
+        // past the row.  Threads 0..127 of the builder warps each build one row.
+        auto build_a = [&](int64_t q0s) {
             // Resident A = complemented unknown rows; zero past the row.  Threads
             // 0..127 each build one row.
             if (!SA && ct < kM) {
-                const int64_t q = q0 + ct;
+                const int64_t q = q0s + ct;
                 const bool real = q < a.n_queries;
                 const int row_words = (int)(a.stride / 4);
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(a.queries + (real ? q : 0) * a.stride);
@@ -619,7 +640,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             } else {
                 ptx::mbar_arrive(a_full);
             }
-        }
+        };
+        if (warp < kBuildWarps) build_a(seg_q0(0));
         if (warp < kFirstEpiWarp) {
         // ---------------- converters ----------------
         // Work unit = (known row, 16-byte half of the stage): 2*BN units per stage.
@@ -685,7 +707,13 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         const int quad = warp & 3;
         const int split = ew >> 2;
         const int m = quad * 32 + lane;
-        const int64_t q = q0 + m;
+        int local = 0;
+        for (int sg = 0; sg < n_seg; ++sg) {
+        // a spare pair's next group: its builders rebuild the unknowns once the
+        // previous group's last accumulator has been read (every MMA reading A is done)
+        if (sg > 0 && warp < kBuildWarps) build_a(seg_q0(sg));
+        const int64_t q0s = seg_q0(sg);
+        const int64_t q = q0s + m;
         const bool q_ok = q < a.n_queries;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
         TopList<KP> top;
@@ -710,7 +738,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         // the min over lists of their KP-th best is far looser.  Recomputed only
         // when this list's best improves (rare).
         const int list_id = slice * kSplits + split;
-        const int n_lists = n_slices * kSplits;
+        const int n_lists = (n_slices + (PAIR && a.n_spare ? 1 : 0)) * kSplits;
         const int n_pub = n_lists < kMinSlots ? n_lists : kMinSlots;
         const bool pub_min = share && a.list_min != nullptr && list_id < kMinSlots && n_pub >= a.k;
         // the k-th smallest published minimum is folded into a.bound by every list
@@ -721,7 +749,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < kAccBufs; ++i) t_empty_leader[i] = ptx::mapa(&t_empty[i], 0);
         }
-        int local = 0;
         for (int64_t t = t_begin; t < t_end; ++t, ++local) {
             const int acc = local % kAccBufs;
             // the shared bound is read before the wait so its latency hides behind it
@@ -860,7 +887,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        ptx::tma_store_2d(&omap, stage, (int)(q0 + quad * 32), (int)r0);
+                        ptx::tma_store_2d(&omap, stage, (int)(q0s + quad * 32), (int)r0);
                         ptx::bulk_commit();
                     }
                     continue;
@@ -922,6 +949,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 empty.store(a.part_scores + off2, a.part_index + off2, a.ref_base);
             }
         }
+        }  // segments
         }
     }
 
@@ -964,6 +992,27 @@ void* launch_scratch(int which, size_t bytes, cudaStream_t stream) {
         slot = {p, bytes};
     }
     return slot.first;
+}
+
+// A side stream (+ fork/join events) per (device, stream) for the spare-pair grid.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream(cudaStream_t stream) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, SideStream> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    SideStream& ss = cache[std::make_pair(dev, stream)];
+    if (!ss.s) {
+        if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+    }
+    return &ss;
 }
 
 // Debug flag 128: host-side phase timings of a launch, printed to stderr.
@@ -1015,6 +1064,28 @@ int num_sms() {
         if (n <= 0) n = 148;
     }
     return n;
+}
+
+// Spare CTA pairs left over by (unknown groups x slices) on this GPU: each
+// takes the tail tiles of groups / n_spare groups.  With S slices, a spare
+// handles `per` groups: equal run times need tail = tiles / (1 + S * per).
+struct SparePlan {
+    int n_spare = 0;
+    int64_t t_main = 0;
+};
+inline SparePlan spare_plan(int64_t n_tiles, int64_t groups, int slices, bool disabled) {
+    SparePlan p;
+    p.t_main = n_tiles;
+    const int64_t pairs = num_sms() / 2;
+    int64_t spare = pairs - groups * slices;
+    if (disabled || spare <= 0 || groups <= 0 || n_tiles < 16 * (slices + 1)) return p;
+    while (spare > 1 && groups % spare) --spare;  // a divisor of the group count
+    const int64_t per = groups / spare;
+    const int64_t tail = n_tiles / (1 + slices * per);
+    if (tail < 1) return p;
+    p.n_spare = (int)spare;
+    p.t_main = n_tiles - tail;
+    return p;
 }
 
 template <int F>
@@ -1139,7 +1210,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     hc.mark("tensor map");
     const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0);
     if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
-    auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR>;
+    auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR, false>;
     FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     hc.mark("set attribute");
     // pairs cover unknowns in groups of 256: prepare A for both halves of the last pair
@@ -1162,14 +1233,18 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     }
     if (PAIR) {
         const int64_t pgroups = ceil_div(a.n_queries, 2 * kM);
-        const int64_t pairs = pgroups * n_slices;
+        const SparePlan sp = spare_plan(tiles, pgroups, n_slices, a.debug_flags & 1024);
+        const int64_t regular = pgroups * n_slices;
+        const int64_t pairs = regular;
         CompareArgs ap = a;
         ap.n_groups = (int)pgroups;
+        ap.n_spare = sp.n_spare;
+        ap.t_main = sp.t_main;
         ap.progress = nullptr;
-        if (2 * pairs <= num_sms()) {  // drift control only among co-resident pairs
-            ap.progress = (int*)launch_scratch(1, (size_t)pairs * sizeof(int), stream);
+        if (2 * (pairs + sp.n_spare) <= num_sms()) {  // drift control only among co-resident pairs
+            ap.progress = (int*)launch_scratch(1, (size_t)regular * sizeof(int), stream);
             if (!ap.progress) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the pair progress counters");
-            FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)pairs * sizeof(int), stream));
+            FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)regular * sizeof(int), stream));
         }
         hc.mark("progress alloc+memset");
         cudaLaunchConfig_t cfg{};
@@ -1184,8 +1259,31 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        SideStream* side = sp.n_spare ? side_stream(stream) : nullptr;
+        if (sp.n_spare) {
+            if (!side) FASTID_FAIL(FASTID_E_CUDA, "cannot create the spare-pair stream");
+            FASTID_CUDA(cudaEventRecord(side->fork, stream));
+        }
         FASTID_CUDA(cudaLaunchKernelEx(&cfg, kern, map, omap, amap, ap, (const uint8_t*)a_global, tiles, n_slices));
         hc.mark("cluster launch");
+        if constexpr (PAIR) if (sp.n_spare) {
+            // The spare pairs: a second grid on a side stream, launched after the regular
+            // one so it lands on the SMs that grid leaves free, joined before anything
+            // that follows on `stream` (the merge).  Its own instantiation keeps the
+            // regular kernel free of the segment loops' registers.
+            auto skern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR, true>;
+            FASTID_CUDA(cudaFuncSetAttribute(skern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
+            CompareArgs as = ap;
+            as.progress = nullptr;
+            as.trace = nullptr;
+            cudaLaunchConfig_t scfg = cfg;
+            scfg.gridDim = dim3((unsigned)(2 * sp.n_spare));
+            scfg.stream = side->s;
+            FASTID_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+            FASTID_CUDA(cudaLaunchKernelEx(&scfg, skern, map, omap, amap, as, (const uint8_t*)a_global, tiles, n_slices));
+            FASTID_CUDA(cudaEventRecord(side->join, side->s));
+            FASTID_CUDA(cudaStreamWaitEvent(stream, side->join, 0));
+        }
     } else {
         kern<<<(unsigned)(groups * n_slices), Roles<F, IMG>::kThreads, lay.total, stream>>>(map, omap, amap, a,
                                                                                          a_global, tiles, n_slices);
@@ -1295,7 +1393,11 @@ int launch_fmt(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t strea
     const int slices = use_pair<F>(a) ? pair_slices_for<F>(a.n_refs, a.n_queries) : slices_for<F>(a.n_refs, a.n_queries);
     if (mode == kFull) return launch_one<F, kFull, 1>(a, slices, stream);
     if (mode == kThreshold) return launch_one<F, kThreshold, 1>(a, slices, stream);
-    *n_parts = kMaxSplits * slices;  // one partial list per (slice, epilogue column split)
+    // one partial list per (slice, epilogue column split), plus the spare pairs' slot
+    *n_parts = kMaxSplits * slices;
+    if (use_pair<F>(a) &&
+        spare_plan(ceil_div(a.n_refs, Fmt<F>::BN), ceil_div(a.n_queries, 2 * kM), slices, a.debug_flags & 1024).n_spare)
+        *n_parts += kMaxSplits;
     switch (a.kpad) {
         case 8: return launch_one<F, kTopK, 8>(a, slices, stream);
         case 16: return launch_one<F, kTopK, 16>(a, slices, stream);
@@ -1332,7 +1434,7 @@ int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation) {
     // an upper bound: the launch reports the partition it used
     if (formulation == FASTID_TENSOR_I8) return kMaxSplits * slices_for<FASTID_TENSOR_I8>(n_refs, n_queries);
     return kMaxSplits * std::max(slices_for<FASTID_TENSOR_F4>(n_refs, n_queries),
-                                 pair_slices_for<FASTID_TENSOR_F4>(n_refs, n_queries));
+                                 pair_slices_for<FASTID_TENSOR_F4>(n_refs, n_queries) + 1);  // + spare slot
 }
 
 int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts, cudaStream_t stream) {

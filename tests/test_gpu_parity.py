@@ -396,8 +396,10 @@ def test_cli_compare_and_search(tmp_path):
 @pytest.mark.parametrize("shape", [(60_000, 2048, 1024), (80_000, 700, 512), (40_000, 1024, 2304)])
 def test_pairs_large_panels(rng, shape):
     """Larger panels on the CTA-pair kernel (resident and streamed unknowns,
-    drift control active): top-k, threshold and full rows near both ends of the
-    known range equal the oracle."""
+    drift control active, and -- where (unknown groups x slices) leaves SMs
+    free -- the spare-pair grid over the tail tiles of several groups): top-k,
+    threshold and full rows near both ends of the known range equal the oracle,
+    and the top-k equals the launch without spare pairs (debug flag 1024)."""
     import torch
 
     m = fb()
@@ -413,6 +415,15 @@ def test_pairs_large_panels(rng, shape):
     pick = np.arange(0, n_q, 7)
     es, ex, _ = oracle.topk(r, q[pick], 16)
     assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex)
+    from paper_1707_00516_b200 import _native
+
+    lib = _native.lib()
+    lib.fastid_debug_flags(1024)
+    try:
+        s2, x2 = db.search_words(q, 16)
+    finally:
+        lib.fastid_debug_flags(0)
+    assert np.array_equal(s, s2) and np.array_equal(x, x2)
     dq = m.DevicePanel.from_words(q, L)
     full = db.full_device(dq)
     rows = np.concatenate([np.arange(0, 64), np.arange(n_r - 300, n_r)])
