@@ -381,7 +381,13 @@ def run_b200(args):
         elapsed = float(t[0])
     comps = args.n_known * args.n_unknown
     value = comps * args.steps / elapsed
-    launches_per_step = 2 + (1 if world > 1 else 0)  # compare kernel + partial merge (+ cross-rank merge)
+    # compare kernel + partial merge (+ cross-rank merge); the mxf4 pair kernel adds a
+    # spare-pair grid when the unknown groups x slices leave SMs free (csrc/tensor.cu spare_plan)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    groups, tiles = -(-args.n_unknown // 256), -(-n_local // 192)
+    slices = max(1, min((sms // 2) // groups, tiles))
+    spare = formulation == "tensor_f4" and (sms // 2) - groups * slices > 0 and tiles >= 16 * (slices + 1)
+    launches_per_step = 2 + (1 if spare else 0) + (1 if world > 1 else 0)
 
     # ---- correctness spot check against the oracle (rank 0, single GPU only)
     verified = None
