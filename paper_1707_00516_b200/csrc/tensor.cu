@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <cstdio>
 #include <map>
@@ -1088,6 +1089,17 @@ inline SparePlan spare_plan(int64_t n_tiles, int64_t groups, int slices, bool di
     return p;
 }
 
+// The spare grid assumes the SMs the regular grid leaves free are idle; on a
+// GPU shared with other work it could start late and lengthen the step, so
+// FASTID_NO_SPARE_PAIRS=1 (or debug flag 1024) turns it off.
+inline bool spares_disabled(const CompareArgs& a) {
+    static const bool env = [] {
+        const char* e = getenv("FASTID_NO_SPARE_PAIRS");
+        return e && *e && *e != '0';
+    }();
+    return env || (a.debug_flags & 1024);
+}
+
 template <int F>
 int slices_for(int64_t n_refs, int64_t n_queries) {
     const int64_t groups = ceil_div(n_queries, kM);
@@ -1233,7 +1245,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     }
     if (PAIR) {
         const int64_t pgroups = ceil_div(a.n_queries, 2 * kM);
-        const SparePlan sp = spare_plan(tiles, pgroups, n_slices, a.debug_flags & 1024);
+        const SparePlan sp = spare_plan(tiles, pgroups, n_slices, spares_disabled(a));
         const int64_t regular = pgroups * n_slices;
         const int64_t pairs = regular;
         CompareArgs ap = a;
@@ -1396,7 +1408,7 @@ int launch_fmt(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t strea
     // one partial list per (slice, epilogue column split), plus the spare pairs' slot
     *n_parts = kMaxSplits * slices;
     if (use_pair<F>(a) &&
-        spare_plan(ceil_div(a.n_refs, Fmt<F>::BN), ceil_div(a.n_queries, 2 * kM), slices, a.debug_flags & 1024).n_spare)
+        spare_plan(ceil_div(a.n_refs, Fmt<F>::BN), ceil_div(a.n_queries, 2 * kM), slices, spares_disabled(a)).n_spare)
         *n_parts += kMaxSplits;
     switch (a.kpad) {
         case 8: return launch_one<F, kTopK, 8>(a, slices, stream);
