@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     constexpr int RB = PAIR ? HB : UB;         // bytes this CTA receives per stage
     constexpr int PB = Layout<F>::kPackedStageBytes;
     using R = Roles<F, IMG>;
-    constexpr int kConvWarps = R::kConvWarps, kConvThreads = 32 * R::kConvWarps;
+    constexpr int kConvThreads = 32 * R::kConvWarps;
     constexpr int kEpiWarps = R::kEpiWarps, kEpiThreads = 32 * R::kEpiWarps;
     constexpr int kBuildWarps = R::kBuildWarps;
     constexpr int kFirstEpiWarp = R::kFirstEpiWarp, kProducerWarp = R::kProducerWarp, kMmaWarp = R::kMmaWarp;
@@ -1115,7 +1115,7 @@ int slices_for(int64_t n_refs, int64_t n_queries) {
 // stage ([group][stage][core matrices]) so each stage is one bulk copy.
 template <int F>
 __global__ void prep_a_kernel(CompareArgs a, int n_groups, int n_kst, uint8_t* __restrict__ out) {
-    constexpr int CPW = Fmt<F>::kCoresPerWord;
+    [[maybe_unused]] constexpr int CPW = Fmt<F>::kCoresPerWord;
     constexpr int AB = Layout<F>::kAStageBytes;
     const int64_t total = (int64_t)n_groups * n_kst * kM;
     const int row_words = (int)(a.stride / 4);
