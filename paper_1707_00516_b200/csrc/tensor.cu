@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 if (tr) a.trace[local * kTrSlots + kTrRel0 + ew] = clock64();
             };
             const uint32_t ta0 = lane_base + col_base;
-            if (kPreload) {
+            if constexpr (kPreload) {
                 // every column of this warp's split in one round of loads, one wait,
                 // the accumulator released at once, then the compare work
                 uint32_t v[kPreBatches][kBatch];
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
                 continue;
-            }
+            } else {
 #pragma unroll
             for (int b0 = 0; b0 < kCols; b0 += kBatch) {
                 if (tr && b0 == kBatch && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
@@ -931,6 +931,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 if (tr && b0 == 0 && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 if (b0 + kBatch >= kCols) release();
                 process(v, b0, nb);
+            }
             }
         }
         if (PAIR && MODE == kFull && a.tma_out && lane == 0) ptx::bulk_wait_all();  // stores done before exit
