@@ -873,6 +873,28 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 release();
+                if (PAIR && MODE == kFull && a.tma_out == 2) {
+                    // full matrix, wide: the 4 lane-quadrant warps of this column split fill
+                    // one [kCols known rows][128 unknowns] block (512-B output rows) and one
+                    // of them issues the TMA tensor store (named barrier per split)
+                    uint32_t* stage = reinterpret_cast<uint32_t*>(smem + lay.off_out) + split * kCols * kM;
+                    const bool issuer = quad == 0 && lane == 0;
+                    if (issuer) ptx::bulk_wait_read0();  // the previous store has read the block
+                    ptx::named_bar_sync(1 + split, 128);
+#pragma unroll
+                    for (int b = 0; b < kPreBatches; ++b)
+#pragma unroll
+                        for (int c = 0; c < kBatch; ++c)
+                            if (b * kBatch + c < kCols)
+                                stage[(b * kBatch + c) * kM + quad * 32 + lane] = decode_fast<F>(v[b][c]);
+                    ptx::fence_proxy_async_smem();
+                    ptx::named_bar_sync(1 + split, 128);
+                    if (issuer) {
+                        ptx::tma_store_2d(&omap, stage, (int)q0s, (int)r0);
+                        ptx::bulk_commit();
+                    }
+                    continue;
+                }
                 if (PAIR && MODE == kFull && a.tma_out) {
                     // full matrix: transpose through this warp's staging block and let a
                     // TMA tensor store write the [kCols known rows][32 unknowns] tile
@@ -1170,12 +1192,12 @@ int make_image_map(CUtensorMap* map, const CompareArgs& a) {
 // Tensor map over the u32 full-matrix output [n_refs][ld_out] (inner dim =
 // unknowns): one box = one epilogue warp's [cols][32] block.  Needs 16-byte
 // alignment of the base and the row pitch.
-int make_out_map(CUtensorMap* map, const CompareArgs& a, int box_cols) {
+int make_out_map(CUtensorMap* map, const CompareArgs& a, int box_cols, int box_unknowns) {
     auto fn = encode_fn();
     if (!fn) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)a.n_queries, (cuuint64_t)a.n_refs};
     cuuint64_t strides[1] = {(cuuint64_t)a.ld_out * 4};
-    cuuint32_t box[2] = {32, (cuuint32_t)box_cols};
+    cuuint32_t box[2] = {(cuuint32_t)box_unknowns, (cuuint32_t)box_cols};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)a.out, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -1211,8 +1233,10 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     a.tma_out = 0;
     if (PAIR && MODE == kFull && a.n_queries > 0 && ((uintptr_t)a.out & 15) == 0 && (a.ld_out * 4) % 16 == 0 &&
         !(a.debug_flags & 256) && Layout<F>(a.stride, SA, IMG, PAIR, out_stage_bytes<F, MODE, IMG, PAIR>()).fits()) {
-        if (int rc = make_out_map(&omap, a, Fmt<F>::BN / (Roles<F, IMG>::kEpiWarps / 4))) return rc;
-        a.tma_out = 1;
+        // wide blocks (128 unknowns = 512-B rows) unless debug flag 2048 asks for the per-warp ones
+        const bool wide = !(a.debug_flags & 2048);
+        if (int rc = make_out_map(&omap, a, Fmt<F>::BN / (Roles<F, IMG>::kEpiWarps / 4), wide ? kM : 32)) return rc;
+        a.tma_out = wide ? 2 : 1;
     }
     CUtensorMap map;
     if (PAIR) {

@@ -17,7 +17,9 @@ nw = L // 64
 rw = torch.randint(-2**62, 2**62, (n_r, nw), dtype=torch.int64, device="cuda", generator=g)
 qw = torch.randint(-2**62, 2**62, (n_q, nw), dtype=torch.int64, device="cuda", generator=g)
 lib = _native.lib()
-for form in ("tensor_f4", "tensor_i8"):
+import os
+lib.fastid_debug_flags(int(os.environ.get("FASTID_FLAGS", "0")))
+for form in (os.environ.get("FASTID_FORMS", "tensor_f4,tensor_i8")).split(","):
     db = KnownDatabase(m.DevicePanel.from_words(rw, L), formulation=form)
     dq = m.DevicePanel.from_words(qw, L)
     out = torch.empty((n_r, n_q), dtype=torch.int32, device="cuda")
