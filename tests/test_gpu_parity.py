@@ -435,3 +435,24 @@ def test_pairs_large_panels(rng, shape):
     hq, hr, hs = oracle.threshold_from_matrix(sub, thr)
     sel = hits.ref >= n_r - 300
     assert np.array_equal(hits.query[sel], hq) and np.array_equal(hits.ref[sel], hr + n_r - 300)
+
+
+@pytest.mark.parametrize("n_r,n_q,k,max_score", [(5, 1, 16, None), (3, 300, 8, 0), (200, 1, 32, 300),
+                                                 (193, 257, 16, None), (1, 2, 1, None)])
+def test_pairs_edge_shapes(rng, n_r, n_q, k, max_score):
+    """Prepared-database (CTA-pair) top-k with fewer knowns than k, a single
+    unknown, a zero or partial score cap, one-row tiles and a second pair group
+    of one unknown: equal to the oracle, empty slots 0xFFFFFFFF / -1."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1024
+    r, _ = rand_words(rng, n_r, 16, 64, L)
+    q, _ = rand_words(rng, n_q, 16, 64, L)
+    q[0] = r[0]  # one exact copy: score 0
+    db = KnownDatabase(r, L, formulation="tensor_f4")
+    s, x = db.search_words(q, k, max_score)
+    es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE if max_score is None else max_score)
+    assert np.array_equal(s, es) and np.array_equal(x, ex)
+    full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, oracle.naive(r, q))
