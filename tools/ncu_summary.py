@@ -24,8 +24,14 @@ print("-- stalls (warps per issue)")
 for v, h in sorted(st, reverse=True)[:8]:
     print(f"  {v:8.3f} {h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}")
 src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
-h = src[1]; rows = src[2:]
+h = src[1]
 ia, isrc, iss, iex = h.index("Address"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+# first kernel of the report only (its rows end where a new header / non-numeric row starts)
+rows = []
+for x in src[2:]:
+    if len(x) != len(h) or not x[iss].strip().isdigit():
+        break
+    rows.append(x)
 tot = sum(int(x[iss]) for x in rows)
 print(f"-- hottest SASS (of {tot} samples)")
 for x in sorted(rows, key=lambda x: -int(x[iss]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
