@@ -456,3 +456,22 @@ def test_pairs_edge_shapes(rng, n_r, n_q, k, max_score):
     assert np.array_equal(s, es) and np.array_equal(x, ex)
     full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
     assert np.array_equal(full, oracle.naive(r, q))
+
+
+def test_database_reuse_across_shapes(rng):
+    """One resident database answering a sequence of batches of different sizes,
+    list sizes and caps (launch scratch, shared bounds, progress counters and the
+    spare-pair stream are reused between calls): every batch equals the oracle."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L, n_r = 1024, 40_000
+    r, _ = rand_words(rng, n_r, 16, 64, L)
+    db = KnownDatabase(r, L, formulation="tensor_f4")
+    for n_q, k, ms in ((2048, 16, None), (1, 1, None), (300, 32, 250), (2048, 5, None), (77, 16, 0)):
+        q, _ = rand_words(rng, n_q, 16, 64, L)
+        q[: max(1, n_q // 9)] = r[rng.integers(0, n_r, max(1, n_q // 9))]
+        s, x = db.search_words(q, k, ms)
+        pick = np.unique(np.linspace(0, n_q - 1, 12).astype(int))
+        es, ex, _ = oracle.topk(r, q[pick], k, 0xFFFFFFFE if ms is None else ms)
+        assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex), (n_q, k, ms)
