@@ -102,8 +102,30 @@ class KnownDatabase:
         self.ref_base = int(ref_base)
         self.formulation = formulation
         self._stagers: dict = {}
-        # the tensor image (built once) lets every query batch skip bit unpacking
-        self.image = PreparedImage(self.panel, formulation) if prepare and self.panel.n_profiles else None
+        # the tensor image (built once) lets every query batch skip bit unpacking; a
+        # database whose image does not fit in device memory (4 bits per locus for
+        # mxf4) keeps only its packed rows and runs the unpacking kernels instead
+        self.image = None
+        if prepare and self.panel.n_profiles:
+            self.image = self._prepare(formulation)
+
+    def _prepare(self, formulation):
+        from .errors import DeviceError
+
+        for attempt in range(2):
+            try:
+                return PreparedImage(self.panel, formulation)
+            except DeviceError as e:
+                if "allocate" not in str(e):
+                    raise
+                if attempt == 0:
+                    torch.cuda.empty_cache()  # cached torch blocks may be what is missing
+                    continue
+                import warnings
+
+                warnings.warn(f"tensor image does not fit on {self.device} ({e}); using packed operands",
+                              RuntimeWarning, stacklevel=3)
+        return None
 
     @property
     def n_profiles(self) -> int:
