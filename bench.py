@@ -293,10 +293,17 @@ def run_b200(args):
     world, rank, local = dist_env()
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; FASTID_DIST_BACKEND=gloo lets a one-GPU box exercise the
+    # multi-rank path (ranks share the device, candidates gathered over gloo)
+    backend = os.environ.get("FASTID_DIST_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _native.lib()
     L = args.loci
     n_words = L // 64
@@ -355,7 +362,7 @@ def run_b200(args):
             s, x = db.topk_device(dq, k, None, ws, out)
         return sharded.combine(s, x, k)
 
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         for _ in range(args.warmup):
             step(False)
         torch.cuda.synchronize()
