@@ -387,9 +387,10 @@ def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int 
                 out: tuple | None = None, events: tuple | None = None, image=None):
     """Fused compare + top-k on the device -> (scores int32 [N_Q, k] as u32, index int64 [N_Q, k]).
 
-    Two launches on the current stream: the comparison kernel (writing
-    per-CTA candidate lists) and the merge kernel.  ``events=(start, end)``
-    are recorded around the comparison kernel alone (roofline timing).
+    On the current stream: the comparison kernel (writing per-CTA candidate
+    lists; with a prepared mxf4 image also the spare-pair grid, forked to a
+    side stream and joined back) and the merge kernel.  ``events=(start, end)``
+    are recorded around the comparison alone (roofline timing).
     """
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
     L = _native.lib()
