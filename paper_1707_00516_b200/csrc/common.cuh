@@ -153,7 +153,7 @@ struct CompareArgs {
     // diagnostics (fastid_debug_trace): CTA 0 timestamps, or null
     long long* trace;
     int trace_tiles;
-    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 1: no CTA pairs; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits; bit 4: no top-k insertions; bit 5: count insertions per tile; bit 6: per-CTA globaltimer stamps; bit 7: host phase timings; bit 8: no TMA-store full matrix; bit 9: weighted (not uniform) mxf4 image encoding; bit 10: no spare CTA pairs; bit 11: per-warp (32-unknown) full-matrix TMA stores (timing experiments only)
+    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 1: no CTA pairs; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits; bit 4: no top-k insertions; bit 5: count insertions per tile; bit 6: per-CTA globaltimer stamps; bit 7: host phase timings; bit 8: no TMA-store full matrix; bit 9: weighted (not uniform) mxf4 image encoding; bit 10: no spare CTA pairs; bit 11: per-warp (32-unknown) full-matrix TMA stores; bit 12: spinning (no suspend hint) accumulator waits; bit 13: spinning producer waits (timing experiments only)
 };
 
 // Per-tile trace slots written by CTA 0 when tracing is on (clock64 values).

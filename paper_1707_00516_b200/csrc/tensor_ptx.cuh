@@ -35,6 +35,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Wait with a suspend-time hint: the thread sleeps in the barrier unit until the
+// phase completes (or the hint expires) instead of re-issuing try_wait -- for
+// warps that wait most of a tile (the epilogue on the accumulator), so the
+// spinning does not cost issue slots and power.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+
 // ---- proxies / TMA ---------------------------------------------------------
 // Make generic-proxy st.shared visible to the async proxy (tensor core reads).
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
