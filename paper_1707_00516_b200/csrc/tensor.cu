@@ -556,10 +556,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 const uint32_t use = (uint32_t)(local / kAccBufs) & 1u;  // parity of this buffer's use
                 const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
                 if (tr) a.trace[local * kTrSlots + kTrMmaWait] = clock64();
-                if (PAIR)
-                    ptx::mbar_wait(&t_empty[acc], use ^ 1);  // spin: MMA wake-up latency is on the critical path
-                else
-                    ptx::mbar_wait(&t_empty[acc], use ^ 1);  // spin: MMA wake-up latency is on the critical path
+                // spinning waits: the MMA warp's wake-up latency is on the critical path
+                ptx::mbar_wait(&t_empty[acc], use ^ 1);
                 if (tr) a.trace[local * kTrSlots + kTrMmaGo] = clock64();
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
