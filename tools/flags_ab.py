@@ -19,7 +19,7 @@ ws = torch.empty(m.compare.topk_workspace_bytes(n_r, n_q, 16, "tensor_f4"), dtyp
 lib = _native.lib()
 FLAG = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 res = {0: [], FLAG: []}
-for rd in range(4):
+for rd in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     for flags in (0, FLAG):
         lib.fastid_debug_flags(flags)
         db.topk_device(dq, 16, None, ws)
