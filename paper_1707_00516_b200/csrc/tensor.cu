@@ -1242,7 +1242,11 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     CUtensorMap omap;
     memset(&omap, 0, sizeof(omap));
     a.tma_out = 0;
-    if (PAIR && MODE == kFull && a.n_queries > 0 && ((uintptr_t)a.out & 15) == 0 && (a.ld_out * 4) % 16 == 0 &&
+    // TMA tensor stores clip out-of-range unknowns only to 16-byte granules (measured:
+    // n_queries = 150 with a wider row pitch wrote columns 150-151), so they are used
+    // only when every granule they touch belongs to the matrix: n_queries % 4 == 0
+    if (PAIR && MODE == kFull && a.n_queries > 0 && a.n_queries % 4 == 0 && ((uintptr_t)a.out & 15) == 0 &&
+        (a.ld_out * 4) % 16 == 0 &&
         !(a.debug_flags & 256) && Layout<F>(a.stride, SA, IMG, PAIR, out_stage_bytes<F, MODE, IMG, PAIR>()).fits()) {
         // wide blocks (128 unknowns = 512-B rows) unless debug flag 2048 asks for the per-warp ones
         const bool wide = !(a.debug_flags & 2048);

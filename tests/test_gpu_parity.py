@@ -8,6 +8,7 @@ import json
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 
@@ -284,6 +285,12 @@ def test_prepared_database_image(rng, form, L):
     full = db.full_device(dq).cpu().numpy().view(np.uint32)
     exp = oracle.naive(r, q)
     assert np.array_equal(full, exp)
+    # every cell is written (the output is poisoned first, so stale allocator
+    # contents cannot pass for results), including a row pitch wider than N_Q
+    poisoned = torch.full((2500, 160), -1, dtype=torch.int32, device=dq.rows.device)
+    db.full_device(dq, poisoned)
+    got = poisoned.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got[:, :150], exp) and (got[:, 150:] == 0xFFFFFFFF).all()
     s, x = db.search_words(q, 16)
     es, ex, _ = oracle.topk_from_matrix(exp, 16)
     assert np.array_equal(s, es)
@@ -475,3 +482,40 @@ def test_database_reuse_across_shapes(rng):
         pick = np.unique(np.linspace(0, n_q - 1, 12).astype(int))
         es, ex, _ = oracle.topk(r, q[pick], k, 0xFFFFFFFE if ms is None else ms)
         assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex), (n_q, k, ms)
+
+
+@pytest.mark.parametrize("n_r,n_q", [(2500, 150), (2500, 152), (2431, 149)])
+def test_full_matrix_writes_stay_in_view(rng, n_r, n_q):
+    """The full matrix is written into a poisoned view [n_r, n_q] of a larger buffer
+    (row pitch 160, 100 extra rows): every cell outside the view keeps the poison,
+    for every formulation, with and without the prepared image and for each epilogue
+    store variant (debug flags 256: no TMA store, 2048: per-warp TMA blocks). Covers
+    the TMA unit's 16-byte clipping of partial unknown granules."""
+    m = fb()
+    from paper_1707_00516_b200 import _native
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1024
+    r, _ = rand_words(rng, n_r, 16, 64, L)
+    q, _ = rand_words(rng, n_q, 16, 64, L)
+    exp = oracle.naive(r, q)
+    dq = m.DevicePanel.from_words(q, L)
+    dr = m.DevicePanel.from_words(r, L)
+    try:
+        for form in ("tensor_f4", "tensor_i8", "popc"):
+            db = KnownDatabase(r, L, formulation=form)
+            for flags in (0, 256, 2048):
+                _native.lib().fastid_debug_flags(flags)
+                for use_db in (True, False):
+                    buf = torch.full((n_r + 100, 160), -1, dtype=torch.int32, device=dq.rows.device)
+                    view = buf[:n_r, :n_q]
+                    if use_db:
+                        db.full_device(dq, view)
+                    else:
+                        m.compare.compare_device(dr, dq, view, form)
+                    g = buf.cpu().numpy().view(np.uint32)
+                    assert np.array_equal(g[:n_r, :n_q], exp), (form, flags, use_db)
+                    g[:n_r, :n_q] = 0xFFFFFFFF
+                    assert (g == 0xFFFFFFFF).all(), (form, flags, use_db, "write outside the view")
+    finally:
+        _native.lib().fastid_debug_flags(0)

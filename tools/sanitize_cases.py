@@ -1,0 +1,63 @@
+"""Small cases over every kernel path, for compute-sanitizer (memcheck / initcheck /
+racecheck / synccheck) on a B200:
+
+    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+
+Each case is checked against the oracle as well, so a run under the sanitizer
+is also a parity run. Sizes are tiny: the sanitizer slows kernels by 100x+.
+"""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+import numpy as np
+import torch
+
+import oracle
+import paper_1707_00516_b200 as fb
+from paper_1707_00516_b200.search import KnownDatabase
+
+
+def panel(rng, n, L, tag):
+    words = rng.integers(0, 2**64, (n, -(-L // 64)), dtype=np.uint64)
+    if L % 64:
+        words[:, -1] &= ~np.uint64(0) << np.uint64(64 - L % 64)
+    return fb.Panel(tuple(f"{tag}{i}" for i in range(n)), words, L)
+
+
+def main():
+    rng = np.random.default_rng(7)
+    n_cases = 0
+    for L, n_r, n_q in ((1024, 600, 96), (127, 300, 33), (5000, 400, 40)):
+        refs, queries = panel(rng, n_r, L, "r"), panel(rng, n_q, L, "q")
+        expected = oracle.naive(refs.words, queries.words)
+        for form in ("popc", "tensor_i8", "tensor_f4"):
+            got = fb.compare_b200(refs, queries, formulation=form).scores
+            assert np.array_equal(got, expected), (L, form, "full")
+            res = fb.topk(refs, queries, 5, formulation=form)
+            s, x, _ = oracle.topk_from_matrix(expected, 5)
+            assert np.array_equal(res.scores, s) and np.array_equal(res.index, x), (L, form, "topk")
+            n_cases += 2
+        db = KnownDatabase(refs)
+        s, x = db.search_words(queries.words, 16)
+        es, ex, _ = oracle.topk_from_matrix(expected, 16)
+        assert np.array_equal(s, es) and np.array_equal(x, ex), (L, "image topk")
+        # poisoned output: bulk-tensor (TMA) stores are invisible to initcheck, so
+        # a value check against the oracle is what proves every cell is written
+        out = torch.full((n_r, n_q), -1, dtype=torch.int32, device="cuda")
+        full = db.full_device(fb.DevicePanel.from_panel(queries), out).cpu().numpy().view(np.uint32)
+        assert np.array_equal(full, expected), (L, "image full")
+        thr = int(np.percentile(expected, 1))
+        hits = db.threshold(queries, thr)
+        jj, ii = np.nonzero(expected.T <= thr)
+        assert np.array_equal(hits.query, jj) and np.array_equal(hits.ref, ii), (L, "threshold hits")
+        assert np.array_equal(hits.score, expected.T[jj, ii]), (L, "threshold scores")
+        n_cases += 3
+    torch.cuda.synchronize()
+    print(f"sanitize cases ok ({n_cases})")
+
+
+if __name__ == "__main__":
+    main()
