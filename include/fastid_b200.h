@@ -92,7 +92,9 @@ FASTID_API int fastid_pack_genotypes(const uint8_t* codes, int64_t rows, int64_t
 /* ---- comparison --------------------------------------------------------- */
 
 /* out[i * ld_out + j] = popcount(refs_i AND NOT queries_j) for all i < n_refs,
- * j < n_queries.  refs / queries are device rows of `stride` bytes. */
+ * j < n_queries.  refs / queries are device rows of `stride` bytes.  `out` may
+ * be a view into a wider matrix (ld_out >= n_queries): no element outside
+ * [0, n_refs) x [0, n_queries) is written. */
 FASTID_API int fastid_compare_full(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
                         int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out,
                         int formulation, void* stream);
