@@ -519,3 +519,52 @@ def test_full_matrix_writes_stay_in_view(rng, n_r, n_q):
                     assert (g == 0xFFFFFFFF).all(), (form, flags, use_db, "write outside the view")
     finally:
         _native.lib().fastid_debug_flags(0)
+
+
+@pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8", "popc"])
+def test_threshold_capacity_overflow(rng, form):
+    """Threshold hits beyond `capacity` are counted but never written past the
+    caller's buffers (poisoned tails stay intact), and threshold_hits' second pass
+    with the exact count returns the oracle's hit list."""
+    m = fb()
+    from paper_1707_00516_b200 import _native
+    from paper_1707_00516_b200.compare import threshold_hits
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1024
+    r, _ = rand_words(rng, 3000, 16, 64, L)
+    q, _ = rand_words(rng, 70, 16, 64, L)
+    exp = oracle.naive(r, q)
+    thr = int(np.percentile(exp, 0.5))
+    jj, ii = np.nonzero(exp.T <= thr)
+    assert len(jj) > 200
+    db = KnownDatabase(r, L, formulation=form)
+    dq = m.DevicePanel.from_words(q, L)
+    cap = 50
+    dev = dq.rows.device
+    for use_db in (True, False):
+        hq = torch.full((cap + 64,), -7, dtype=torch.int32, device=dev)
+        hr = torch.full((cap + 64,), -7, dtype=torch.int64, device=dev)
+        hs = torch.full((cap + 64,), -7, dtype=torch.int32, device=dev)
+        count = torch.zeros(1, dtype=torch.int64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        if use_db:
+            rc = _native.lib().fastid_db_compare_threshold(
+                db.image.handle, dq.rows.data_ptr(), dq.n_profiles, thr, 0,
+                hq.data_ptr(), hr.data_ptr(), hs.data_ptr(), cap, count.data_ptr(), stream)
+        else:
+            dr = db.panel
+            rc = _native.lib().fastid_compare_threshold(
+                dr.rows.data_ptr(), dr.n_profiles, dq.rows.data_ptr(), dq.n_profiles, dr.stride, dr.bit_length, thr,
+                0, hq.data_ptr(), hr.data_ptr(), hs.data_ptr(), cap, count.data_ptr(),
+                _native.formulation_code(form), stream)
+        assert rc == 0, _native.lib().fastid_last_error()
+        torch.cuda.synchronize()
+        assert int(count.item()) == len(jj)
+        assert (hq[cap:] == -7).all() and (hr[cap:] == -7).all() and (hs[cap:] == -7).all()
+        # the written prefix holds genuine hits
+        got = set(zip(hq[:cap].cpu().tolist(), hr[:cap].cpu().tolist()))
+        assert got <= set(zip(jj.tolist(), ii.tolist()))
+    res = threshold_hits(db.panel, dq, thr, capacity=cap, formulation=form)
+    assert np.array_equal(res.query, jj) and np.array_equal(res.ref, ii)
+    assert np.array_equal(res.score, exp.T[jj, ii])
