@@ -568,3 +568,33 @@ def test_threshold_capacity_overflow(rng, form):
     res = threshold_hits(db.panel, dq, thr, capacity=cap, formulation=form)
     assert np.array_equal(res.query, jj) and np.array_equal(res.ref, ii)
     assert np.array_equal(res.score, exp.T[jj, ii])
+
+
+@pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8", "popc"])
+def test_topk_writes_stay_in_workspace(rng, form):
+    """Top-k with exactly the advertised workspace (a view into a poisoned larger
+    buffer) and output views: nothing past the workspace or outside the outputs is
+    written. 600 unknowns = 3 pair groups, so the mxf4 path also runs the spare-pair
+    grid (its list slot is part of the advertised size)."""
+    m = fb()
+    from paper_1707_00516_b200.compare import topk_workspace_bytes
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L, n_r, n_q, k = 1024, 100_000, 600, 16
+    r, _ = rand_words(rng, n_r, 16, 64, L)
+    q, _ = rand_words(rng, n_q, 16, 64, L)
+    q[:40] = r[rng.integers(0, n_r, 40)]
+    db = KnownDatabase(r, L, formulation=form)
+    dq = m.DevicePanel.from_words(q, L)
+    dev = dq.rows.device
+    need = topk_workspace_bytes(n_r, n_q, k, form)
+    ws_full = torch.full((need + 8192,), 0xAB, dtype=torch.uint8, device=dev)
+    s_full = torch.full((n_q + 8, k), -7, dtype=torch.int32, device=dev)
+    x_full = torch.full((n_q + 8, k), -7, dtype=torch.int64, device=dev)
+    out = (s_full[:n_q], x_full[:n_q])
+    s, x = db.topk_device(dq, k, None, ws_full[:need], out)
+    torch.cuda.synchronize()
+    assert (ws_full[need:] == 0xAB).all(), "write past the advertised workspace"
+    assert (s_full[n_q:] == -7).all() and (x_full[n_q:] == -7).all(), "write past the outputs"
+    es, ex, _ = oracle.topk(r, q, k)
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), es) and np.array_equal(x.cpu().numpy(), ex)
