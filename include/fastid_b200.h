@@ -153,6 +153,20 @@ FASTID_API int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride
 FASTID_API int fastid_db_destroy(fastid_db* db);
 FASTID_API int fastid_db_formulation(const fastid_db* db);
 
+/* Execution variants of a prepared database.  Every option computes the same
+ * result (bit-exact); they only select among kernel paths, so tests can reach
+ * each one.  Options apply to later calls on this handle only. */
+enum fastid_db_option {
+    FASTID_OPT_NO_CTA_PAIRS = 1,      /* single-CTA kernel instead of CTA pairs       */
+    FASTID_OPT_NO_TMA_STORE = 2,      /* full matrix by per-element stores            */
+    FASTID_OPT_NO_SPARE_PAIRS = 4,    /* no spare-pair grid on the SMs left over      */
+    FASTID_OPT_NARROW_TMA_STORE = 8   /* per-warp (32-unknown) TMA-store blocks       */
+};
+/* Set (value != 0) or clear one FASTID_OPT_* bit of the handle. */
+FASTID_API int fastid_db_set_option(fastid_db* db, int option, int value);
+/* The handle's current FASTID_OPT_* bits (-1 for NULL). */
+FASTID_API int fastid_db_options(const fastid_db* db);
+
 /* As fastid_compare_full / fastid_topk_partials / fastid_compare_threshold with
  * the database's refs, stride, bit_length and formulation. */
 FASTID_API int fastid_db_compare_full(const fastid_db* db, const void* queries, int64_t n_queries,
@@ -197,16 +211,14 @@ FASTID_API int fastid_run_kernel_fd(const void* ref_words, int64_t n_refs, const
 FASTID_API int fastid_probe_peak(int formulation, int iters, void* scratch, double* work, void* stream);
 /* Diagnostic variants of the tensor probe (variant bit 0: one accumulator for
  * every MMA; bit 1: concurrent 28 KB bulk copies from `src` into shared memory). */
-/* Diagnostic: trace CTA 0 of subsequent tensor launches (35 clock64 stamps per
- * tile for the first `tiles` tiles; see TraceSlot in csrc/common.cuh); NULL = off. */
-FASTID_API int fastid_debug_trace(long long* device_buf, int tiles);
-/* Diagnostic: timing-experiment switches (bit 0: epilogue skips TMEM loads; results invalid). */
-FASTID_API int fastid_debug_flags(int flags);
 FASTID_API int fastid_probe_tmem_read(int x, int warps, int iters, void* scratch, double* work, void* stream);
 /* Diagnostic: MMA stream concurrent with `readers` warps of TMEM loads; sink = 2*SMs u64. */
 FASTID_API int fastid_probe_contention(int iters, int readers, void* sink, void* stream);
 FASTID_API int fastid_probe_variant(int formulation, int variant, int iters, void* scratch, const void* src,
                                     int64_t src_bytes, double* work, void* stream);
+/* Timing-experiment switches and per-tile traces are not part of this library:
+ * they exist only in the separate experiments build (_fastid_b200_diag.so,
+ * include/fastid_b200_diag.h). */
 
 /* ---- bulk panel ingest (host) ------------------------------------------- */
 

@@ -35,8 +35,9 @@ import numpy as np
 import torch
 
 from . import _native
-from .errors import CodecError, PanelMismatchError
-from .panel import Panel, QueryLayout, ScoreMatrix, ThresholdHits, TileConfig, TopKResult, word_dtype
+from .errors import CodecError, CorruptProfileError, PanelMismatchError
+from .panel import (Panel, QueryLayout, ScoreMatrix, ThresholdHits, TileConfig, TopKResult, padding_mask, word_dtype,
+                    words_per_profile)
 
 __all__ = [
     "DevicePanel",
@@ -113,20 +114,41 @@ class DevicePanel:
 
     @classmethod
     def from_words(cls, words, bit_length: int, ids=None, device=None) -> "DevicePanel":
-        """Upload a (N, N_W) u32/u64 word array (host numpy or CUDA tensor)."""
-        dev = _require_cuda(device)
-        if isinstance(words, torch.Tensor):
-            if words.dtype not in (torch.int32, torch.int64, torch.uint32, torch.uint64):
-                raise ValueError("word tensors must be 32- or 64-bit integers")
+        """Upload a (N, N_W) u32/u64 word array (host numpy or CUDA tensor).
+
+        The words are validated as the reference Panel validates them
+        (kernel.py:60-63, 85-90): exactly ceil(L/B) words per row (ValueError)
+        and zero padding past bit L (CorruptProfileError) -- before any device work.
+        """
+        if bit_length <= 0:
+            raise ValueError("panel bit length must be positive")
+        is_tensor = isinstance(words, torch.Tensor)
+        if is_tensor:
+            if words.dtype not in (torch.int32, torch.int64, torch.uint32, torch.uint64) or words.dim() != 2:
+                raise ValueError("word tensors must be 2-D 32- or 64-bit integers")
             width = words.element_size() * 8
-            src = words.to(dev).contiguous()
-            n, n_words = src.shape
+            n, n_words = words.shape
         else:
             arr = np.ascontiguousarray(words)
             if arr.dtype not in (np.uint32, np.uint64) or arr.ndim != 2:
                 raise ValueError("word arrays must be 2-D uint32/uint64")
             width = arr.dtype.itemsize * 8
             n, n_words = arr.shape
+        need = words_per_profile(bit_length, width)
+        if n_words != need:
+            raise ValueError(f"expected {need} words for {bit_length} bits at width {width}, got {n_words}")
+        mask = padding_mask(bit_length, width)
+        if mask and n and not is_tensor and np.any(arr[:, -1] & arr.dtype.type(mask)):
+            raise CorruptProfileError(f"nonzero padding past bit {bit_length}")
+        dev = _require_cuda(device)
+        if is_tensor:
+            src = words.to(dev).contiguous()
+            # the tensor holds the words' bits as (possibly signed) integers: mask in that type
+            m = mask - (1 << width) if mask >= 1 << (width - 1) else mask
+            signed = src.view(torch.int64 if width == 64 else torch.int32)
+            if mask and n and bool((signed[:, -1] & m).any()):
+                raise CorruptProfileError(f"nonzero padding past bit {bit_length}")
+        else:
             raw = arr.view(np.uint8).reshape(n, -1) if n else np.zeros((0, n_words * width // 8), np.uint8)
             if not raw.flags.writeable:
                 raw = raw.copy()

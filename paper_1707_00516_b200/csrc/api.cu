@@ -3,6 +3,7 @@
 // drop-in behind fastid_run_kernel.
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cerrno>
 #include <condition_variable>
@@ -32,6 +33,18 @@ void set_error(const char* fmt, ...) {
 
 const char* get_error() { return g_error.c_str(); }
 
+int num_sms() {
+    static std::atomic<int> cached{0};
+    int n = cached.load(std::memory_order_relaxed);
+    if (!n) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cached.store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
 namespace {
 
 int list_size_for(int k) { return k <= 8 ? 8 : (k <= 16 ? 16 : 32); }
@@ -60,16 +73,21 @@ int check_compare(const void* refs, int64_t n_refs, const void* queries, int64_t
     return FASTID_OK;
 }
 
+#ifdef FASTID_EXPERIMENTS
+// experiments build only (include/fastid_b200_diag.h): process-global switches
 long long* g_trace = nullptr;
 int g_trace_tiles = 0;
 int g_debug_flags = 0;
+#endif
 
 CompareArgs make_args(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries, int64_t stride,
                       int64_t bit_length) {
     CompareArgs a{};
+#ifdef FASTID_EXPERIMENTS
     a.trace = g_trace;
     a.trace_tiles = g_trace_tiles;
     a.debug_flags = g_debug_flags;
+#endif
     a.refs = (const uint8_t*)refs;
     a.queries = (const uint8_t*)queries;
     a.n_refs = n_refs;
@@ -204,25 +222,31 @@ struct HostContext {
             if (!h2d_done[i] && cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming) != cudaSuccess)
                 FASTID_FAIL(FASTID_E_CUDA, "cudaEventCreate failed");
         }
-        if (in_bytes > pin_in_cap || out_bytes > pin_out_cap) {
+        // A failed allocation leaves both slots of that buffer freed and its
+        // capacity 0, so a later call reallocates instead of using a null slot.
+        auto grow_pinned = [&](void** slots, size_t& cap, size_t bytes) -> int {
+            if (bytes <= cap) return FASTID_OK;
             cudaStreamSynchronize(stream);
             for (int i = 0; i < 2; ++i) {
-                if (in_bytes > pin_in_cap) {
-                    if (pin_in[i]) cudaFreeHost(pin_in[i]);
-                    pin_in[i] = nullptr;
-                    if (cudaMallocHost(&pin_in[i], in_bytes) != cudaSuccess)
-                        FASTID_FAIL(FASTID_E_NOMEM, "cudaMallocHost of %zu bytes failed", in_bytes);
-                }
-                if (out_bytes > pin_out_cap) {
-                    if (pin_out[i]) cudaFreeHost(pin_out[i]);
-                    pin_out[i] = nullptr;
-                    if (cudaMallocHost(&pin_out[i], out_bytes) != cudaSuccess)
-                        FASTID_FAIL(FASTID_E_NOMEM, "cudaMallocHost of %zu bytes failed", out_bytes);
+                if (slots[i]) cudaFreeHost(slots[i]);
+                slots[i] = nullptr;
+            }
+            cap = 0;
+            for (int i = 0; i < 2; ++i) {
+                if (cudaMallocHost(&slots[i], bytes) != cudaSuccess) {
+                    cudaGetLastError();
+                    for (int j = 0; j < 2; ++j) {
+                        if (slots[j]) cudaFreeHost(slots[j]);
+                        slots[j] = nullptr;
+                    }
+                    FASTID_FAIL(FASTID_E_NOMEM, "cudaMallocHost of %zu bytes failed", bytes);
                 }
             }
-            if (in_bytes > pin_in_cap) pin_in_cap = in_bytes;
-            if (out_bytes > pin_out_cap) pin_out_cap = out_bytes;
-        }
+            cap = bytes;
+            return FASTID_OK;
+        };
+        if (int rc = grow_pinned(pin_in, pin_in_cap, in_bytes)) return rc;
+        if (int rc = grow_pinned(pin_out, pin_out_cap, out_bytes)) return rc;
         const size_t want[3] = {raw_bytes, rows_bytes, out_bytes};
         for (int j = 0; j < 3; ++j) {
             if (want[j] <= dev_slot_cap[j]) continue;
@@ -230,8 +254,15 @@ struct HostContext {
             for (int i = 0; i < 2; ++i) {
                 if (dev_slot[i][j]) cudaFree(dev_slot[i][j]);
                 dev_slot[i][j] = nullptr;
+            }
+            dev_slot_cap[j] = 0;
+            for (int i = 0; i < 2; ++i) {
                 if (cudaMalloc(&dev_slot[i][j], want[j]) != cudaSuccess) {
                     cudaGetLastError();
+                    for (int m = 0; m < 2; ++m) {
+                        if (dev_slot[m][j]) cudaFree(dev_slot[m][j]);
+                        dev_slot[m][j] = nullptr;
+                    }
                     FASTID_FAIL(FASTID_E_NOMEM, "cudaMalloc of %zu bytes failed", want[j]);
                 }
             }
@@ -304,19 +335,23 @@ using namespace fastid;
 
 extern "C" int fastid_abi_version(void) { return FASTID_ABI_VERSION; }
 
-// Diagnostics: subsequent tensor launches record, in CTA 0, kTrSlots clock64()
-// stamps per tile for the first `tiles` tiles into `device_buf` (null = off).
-extern "C" int fastid_debug_trace(long long* device_buf, int tiles) {
+#ifdef FASTID_EXPERIMENTS
+// Diagnostics (experiments build only): subsequent tensor launches record, in
+// CTA 0, kTrSlots clock64() stamps per tile for the first `tiles` tiles into
+// `device_buf` (null = off).
+extern "C" FASTID_API int fastid_debug_trace(long long* device_buf, int tiles) {
     g_trace = device_buf;
     g_trace_tiles = device_buf ? tiles : 0;
     return FASTID_OK;
 }
 
-// Diagnostics: timing-experiment switches for subsequent launches (0 = normal).
-extern "C" int fastid_debug_flags(int flags) {
+// Diagnostics (experiments build only): timing-experiment switches for
+// subsequent launches (0 = normal).
+extern "C" FASTID_API int fastid_debug_flags(int flags) {
     g_debug_flags = flags;
     return FASTID_OK;
 }
+#endif
 extern "C" const char* fastid_last_error(void) { return get_error(); }
 extern "C" int64_t fastid_row_stride(int64_t bit_length) { return bit_length > 0 ? row_stride_bytes(bit_length) : 0; }
 extern "C" int fastid_max_k(void) { return kMaxTopK; }
@@ -327,7 +362,7 @@ extern "C" int fastid_supports(int formulation, int64_t bit_length) {
 }
 
 namespace {
-int compare_full_impl(const void* refs, const void* image, int64_t n_refs, const void* queries, int64_t n_queries,
+int compare_full_impl(const void* refs, const void* image, int options, int64_t n_refs, const void* queries, int64_t n_queries,
                       int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out, int formulation,
                       void* stream) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
@@ -335,6 +370,7 @@ int compare_full_impl(const void* refs, const void* image, int64_t n_refs, const
     if (n_refs == 0 || n_queries == 0) return FASTID_OK;
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
     a.image = (const uint8_t*)image;
+    a.options = options;
     a.out = out;
     a.ld_out = ld_out;
     int parts = 0;
@@ -345,7 +381,7 @@ int compare_full_impl(const void* refs, const void* image, int64_t n_refs, const
 extern "C" int fastid_compare_full(const void* refs, int64_t n_refs, const void* queries, int64_t n_queries,
                                    int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out,
                                    int formulation, void* stream) {
-    return compare_full_impl(refs, nullptr, n_refs, queries, n_queries, stride, bit_length, out, ld_out, formulation,
+    return compare_full_impl(refs, nullptr, 0, n_refs, queries, n_queries, stride, bit_length, out, ld_out, formulation,
                              stream);
 }
 
@@ -368,7 +404,7 @@ extern "C" int fastid_topk_workspace(int64_t n_refs, int64_t n_queries, int k, i
 }
 
 namespace {
-int topk_partials_impl(const void* refs, const void* image, int64_t n_refs, const void* queries, int64_t n_queries,
+int topk_partials_impl(const void* refs, const void* image, int options, int64_t n_refs, const void* queries, int64_t n_queries,
                        int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
                        void* workspace, size_t workspace_bytes, int formulation, void* stream, int* n_lists,
                        int* list_len, size_t* index_offset, size_t* score_offset) {
@@ -386,6 +422,7 @@ int topk_partials_impl(const void* refs, const void* image, int64_t n_refs, cons
     const int parts = parts_for(f, n_refs, n_queries);
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
     a.image = (const uint8_t*)image;
+    a.options = options;
     a.k = k;
     a.kpad = kp;
     a.max_score = max_score;
@@ -412,7 +449,7 @@ extern "C" int fastid_topk_partials(const void* refs, int64_t n_refs, const void
                                     int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
                                     void* workspace, size_t workspace_bytes, int formulation, void* stream,
                                     int* n_lists, int* list_len, size_t* index_offset, size_t* score_offset) {
-    return topk_partials_impl(refs, nullptr, n_refs, queries, n_queries, stride, bit_length, k, max_score, ref_base,
+    return topk_partials_impl(refs, nullptr, 0, n_refs, queries, n_queries, stride, bit_length, k, max_score, ref_base,
                               workspace, workspace_bytes, formulation, stream, n_lists, list_len, index_offset,
                               score_offset);
 }
@@ -440,7 +477,7 @@ extern "C" int fastid_compare_topk(const void* refs, int64_t n_refs, const void*
 }
 
 namespace {
-int threshold_impl(const void* refs, const void* image, int64_t n_refs, const void* queries, int64_t n_queries,
+int threshold_impl(const void* refs, const void* image, int options, int64_t n_refs, const void* queries, int64_t n_queries,
                    int64_t stride, int64_t bit_length, uint32_t threshold, int64_t ref_base, uint32_t* hit_query,
                    int64_t* hit_ref, uint32_t* hit_score, int64_t capacity, unsigned long long* hit_count,
                    int formulation, void* stream) {
@@ -451,6 +488,7 @@ int threshold_impl(const void* refs, const void* image, int64_t n_refs, const vo
     if (n_refs == 0 || n_queries == 0) return FASTID_OK;
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
     a.image = (const uint8_t*)image;
+    a.options = options;
     a.threshold = threshold;
     a.ref_base = ref_base;
     a.hit_query = hit_query;
@@ -468,7 +506,7 @@ extern "C" int fastid_compare_threshold(const void* refs, int64_t n_refs, const 
                                         uint32_t* hit_query, int64_t* hit_ref, uint32_t* hit_score,
                                         int64_t capacity, unsigned long long* hit_count, int formulation,
                                         void* stream) {
-    return threshold_impl(refs, nullptr, n_refs, queries, n_queries, stride, bit_length, threshold, ref_base,
+    return threshold_impl(refs, nullptr, 0, n_refs, queries, n_queries, stride, bit_length, threshold, ref_base,
                           hit_query, hit_ref, hit_score, capacity, hit_count, formulation, stream);
 }
 
@@ -481,6 +519,7 @@ struct fastid_db {
     void* image;      // owned; null for the CUDA-core formulation
     size_t image_bytes;
     int device;
+    int options;  // FASTID_OPT_* bits
 };
 
 extern "C" size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation) {
@@ -495,7 +534,7 @@ extern "C" int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride
     *out = nullptr;
     if (int rc = check_compare(refs, n_refs, refs, 0, stride, bit_length, formulation)) return rc;
     auto* db = new fastid_db{refs, n_refs, stride, bit_length, resolve_formulation(formulation, bit_length),
-                             nullptr, 0, 0};
+                             nullptr, 0, 0, 0};
     cudaGetDevice(&db->device);
     if (db->formulation != FASTID_POPC && n_refs > 0) {
         db->image_bytes = tensor_image_bytes(n_refs, bit_length, db->formulation);
@@ -531,10 +570,23 @@ extern "C" int fastid_db_destroy(fastid_db* db) {
 
 extern "C" int fastid_db_formulation(const fastid_db* db) { return db ? db->formulation : -1; }
 
+constexpr int kAllOptions =
+    FASTID_OPT_NO_CTA_PAIRS | FASTID_OPT_NO_TMA_STORE | FASTID_OPT_NO_SPARE_PAIRS | FASTID_OPT_NARROW_TMA_STORE;
+
+extern "C" int fastid_db_set_option(fastid_db* db, int option, int value) {
+    if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    if (option == 0 || (option & ~kAllOptions) || (option & (option - 1)))
+        FASTID_FAIL(FASTID_E_INVALID, "unknown database option %d", option);
+    db->options = value ? (db->options | option) : (db->options & ~option);
+    return FASTID_OK;
+}
+
+extern "C" int fastid_db_options(const fastid_db* db) { return db ? db->options : -1; }
+
 extern "C" int fastid_db_compare_full(const fastid_db* db, const void* queries, int64_t n_queries, uint32_t* out,
                                       int64_t ld_out, void* stream) {
     if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
-    return compare_full_impl(db->refs, db->image, db->n_refs, queries, n_queries, db->stride, db->bit_length, out,
+    return compare_full_impl(db->refs, db->image, db->options, db->n_refs, queries, n_queries, db->stride, db->bit_length, out,
                              ld_out, db->formulation, stream);
 }
 
@@ -543,7 +595,7 @@ extern "C" int fastid_db_topk_partials(const fastid_db* db, const void* queries,
                                        void* stream, int* n_lists, int* list_len, size_t* index_offset,
                                        size_t* score_offset) {
     if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
-    return topk_partials_impl(db->refs, db->image, db->n_refs, queries, n_queries, db->stride, db->bit_length, k,
+    return topk_partials_impl(db->refs, db->image, db->options, db->n_refs, queries, n_queries, db->stride, db->bit_length, k,
                               max_score, ref_base, workspace, workspace_bytes, db->formulation, stream, n_lists,
                               list_len, index_offset, score_offset);
 }
@@ -553,7 +605,7 @@ extern "C" int fastid_db_compare_threshold(const fastid_db* db, const void* quer
                                            int64_t* hit_ref, uint32_t* hit_score, int64_t capacity,
                                            unsigned long long* hit_count, void* stream) {
     if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
-    return threshold_impl(db->refs, db->image, db->n_refs, queries, n_queries, db->stride, db->bit_length, threshold,
+    return threshold_impl(db->refs, db->image, db->options, db->n_refs, queries, n_queries, db->stride, db->bit_length, threshold,
                           ref_base, hit_query, hit_ref, hit_score, capacity, hit_count, db->formulation, stream);
 }
 
@@ -585,7 +637,7 @@ int run_host(const void* ref_words, int64_t n_refs, const void* query_words, int
     FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], query_words, q_in, cudaMemcpyHostToDevice, st));
     if (queries_transposed) {
         const int64_t work = n_queries * (stride / 4);
-        transpose_words_kernel<<<(unsigned)(work < 148 * 64 * 32 ? ceil_div(work, 256) : 148 * 32), 256, 0, st>>>(
+        transpose_words_kernel<<<(unsigned)std::min<int64_t>(ceil_div(work, 256), num_sms() * 32), 256, 0, st>>>(
             (const uint8_t*)ctx->buf[0], n_words, n_queries, wb, (uint8_t*)ctx->buf[2], stride);
         FASTID_LAUNCHED("transpose_words_kernel");
     } else if (int rc = fastid_load_words(ctx->buf[0], n_queries, row_bytes, ctx->buf[2], stride, st)) {

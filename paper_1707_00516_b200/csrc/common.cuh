@@ -38,6 +38,7 @@ const char* get_error();
     } while (0)
 
 constexpr int kMaxTopK = 32;
+constexpr int kMaxMergeLists = 768;  // candidate lists one merge folds per unknown (merge.cu)
 constexpr int kMinSlots = 32;  // lists per unknown that publish their best value (shared top-k bound)
 constexpr uint32_t kEmptyScore = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyLocal = 0xFFFFFFFFu;
@@ -45,6 +46,9 @@ constexpr uint32_t kEmptyLocal = 0xFFFFFFFFu;
 inline int64_t row_stride_bytes(int64_t bit_length) { return ((bit_length + 127) / 128) * 16; }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Streaming multiprocessors of the current device (148 on a B200), cached.
+int num_sms();
 
 // (score, index) lexicographic order: the canonical tie-break of every top-k
 // output (score ascending, then known index ascending).
@@ -150,11 +154,32 @@ struct CompareArgs {
     uint32_t* hit_score;
     int64_t capacity;
     unsigned long long* hit_count;
-    // diagnostics (fastid_debug_trace): CTA 0 timestamps, or null
-    long long* trace;
+    // Execution variants of a prepared database (fastid_db_set_option): every
+    // one computes the same result; they select among kernel paths
+    // (FASTID_OPT_* bits, include/fastid_b200.h).
+    int options;
+    // Diagnostics.  Only the experiments build (-DFASTID_EXPERIMENTS,
+    // _fastid_b200_diag.so, include/fastid_b200_diag.h) reads these; in the
+    // product library every branch on them is compiled out (see experiment()).
+    long long* trace;  // CTA 0 timestamps, or null
     int trace_tiles;
-    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 1: no CTA pairs; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits; bit 4: no top-k insertions; bit 5: count insertions per tile; bit 6: per-CTA globaltimer stamps; bit 7: host phase timings; bit 8: no TMA-store full matrix; bit 9: weighted (not uniform) mxf4 image encoding; bit 10: no spare CTA pairs; bit 11: per-warp (32-unknown) full-matrix TMA stores; bit 12: spinning (no suspend hint) accumulator waits; bit 13: spinning producer waits (timing experiments only)
+    int debug_flags;  // bit 0: epilogue skips TMEM loads; bit 2: pairs skip operand loads; bit 3: trace MMA stage waits; bit 4: no top-k insertions; bit 5: count insertions per tile; bit 6: per-CTA globaltimer stamps; bit 7: host phase timings; bit 9: weighted (not uniform) mxf4 image encoding; bit 12: spinning (no suspend hint) accumulator waits; bit 13: spinning producer waits (timing experiments only; several invalidate results)
 };
+
+#ifdef FASTID_EXPERIMENTS
+constexpr bool kExperiments = true;
+#else
+constexpr bool kExperiments = false;
+#endif
+
+// Experiment switch `bit` of a launch: always false in the product library.
+__host__ __device__ __forceinline__ bool experiment(const CompareArgs& a, int bit) {
+    return kExperiments && (a.debug_flags & bit) != 0;
+}
+// Diagnostic trace buffer of a launch: always null in the product library.
+__host__ __device__ __forceinline__ long long* trace_buf(const CompareArgs& a) {
+    return kExperiments ? a.trace : nullptr;
+}
 
 // Per-tile trace slots written by CTA 0 when tracing is on (clock64 values).
 enum TraceSlot {

@@ -80,7 +80,7 @@ __global__ void pack_kernel(Src src, int64_t rows, int64_t bit_length, int word_
 
 int grid_for(int64_t work) {
     int64_t blocks = (work + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > num_sms() * 32) blocks = num_sms() * 32;
     return (int)(blocks < 1 ? 1 : blocks);
 }
 

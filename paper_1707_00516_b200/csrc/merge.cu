@@ -75,8 +75,9 @@ __global__ void merge_kernel(const uint32_t* __restrict__ cs, const int64_t* __r
 
 int launch_merge(const uint32_t* cs, const int64_t* ci, int n_lists, int64_t n_queries, int k_in, int k,
                  uint32_t* out_s, int64_t* out_i, cudaStream_t stream) {
-    if (n_lists < 1 || n_lists > 32 * kMaxListsPerLane)
-        FASTID_FAIL(FASTID_E_INVALID, "n_lists must be in [1, %d], got %d", 32 * kMaxListsPerLane, n_lists);
+    static_assert(32 * kMaxListsPerLane == kMaxMergeLists, "merge capacity");
+    if (n_lists < 1 || n_lists > kMaxMergeLists)
+        FASTID_FAIL(FASTID_E_INVALID, "n_lists must be in [1, %d], got %d", kMaxMergeLists, n_lists);
     if (k < 1 || k_in < 1) FASTID_FAIL(FASTID_E_INVALID, "k must be positive");
     if (n_queries == 0) return FASTID_OK;
     const int64_t threads = n_queries * 32;

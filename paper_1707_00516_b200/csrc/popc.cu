@@ -196,10 +196,14 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
 }  // namespace
 
 int popc_parts(int64_t n_refs, int64_t n_queries) {
-    // Enough (group, slice) CTAs for ~2 waves at 2 CTAs/SM.
+    // Enough (group, slice) CTAs for ~2 waves at 2 CTAs/SM, and at most one
+    // wave's worth of slices per group: each slice writes two partial lists
+    // and the merge folds at most 768 lists per unknown (merge.cu).
     const int64_t groups = ceil_div(n_queries, kRows);
     const int64_t tiles = ceil_div(n_refs, kRows);
-    int64_t slices = ceil_div(2 * 2 * 148, groups);
+    int64_t slices = ceil_div(2 * 2 * num_sms(), groups);
+    if (slices > 2 * num_sms()) slices = 2 * num_sms();
+    if (slices > kMaxMergeLists / 2) slices = kMaxMergeLists / 2;
     if (slices > tiles) slices = tiles;
     if (slices < 1) slices = 1;
     return (int)slices * 2;  // two partial lists per slice (one per half-CTA)

@@ -125,7 +125,7 @@ __device__ __forceinline__ uint4 unpack_f4_uniform(uint32_t w) {
 // ahead of the MMA, so its wake-up latency is hidden; sleeping instead of
 // re-issuing try_wait lowers power under the cap): ~1% on C3.
 __device__ __forceinline__ void producer_wait(const CompareArgs& a, uint64_t* bar, uint32_t parity) {
-    if (a.debug_flags & 8192)
+    if (experiment(a, 8192))
         ptx::mbar_wait(bar, parity);
     else
         ptx::mbar_wait_sleep(bar, parity);
@@ -133,7 +133,7 @@ __device__ __forceinline__ void producer_wait(const CompareArgs& a, uint64_t* ba
 
 // debug flag 512 keeps the weighted encoding for the image too (A/B timing; image and
 // queries must be prepared under the same setting)
-__device__ __forceinline__ bool uniform_image(const CompareArgs& a) { return !(a.debug_flags & 512); }
+__device__ __forceinline__ bool uniform_image(const CompareArgs& a) { return !experiment(a, 512); }
 
 template <bool B_SIDE>
 __device__ __forceinline__ void unpack_i8(uint32_t w, uint4& lo, uint4& hi) {
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    if ((a.debug_flags & 64) && a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 4] = (long long)ptx::globaltimer();
+    if (experiment(a, 64) && trace_buf(a) && threadIdx.x == 0) trace_buf(a)[blockIdx.x * 4] = (long long)ptx::globaltimer();
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // CTA pair or CTA
@@ -422,8 +422,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // debug flag 64: per-CTA %globaltimer stamps (entry, roles start, roles done, exit)
-    const bool cta_trace = (a.debug_flags & 64) && a.trace && threadIdx.x == 0;
-    if (cta_trace) a.trace[blockIdx.x * 4 + 1] = (long long)ptx::globaltimer();
+    const bool cta_trace = experiment(a, 64) && trace_buf(a) && threadIdx.x == 0;
+    if (cta_trace) trace_buf(a)[blockIdx.x * 4 + 1] = (long long)ptx::globaltimer();
     if (F == FASTID_TENSOR_F4 && warp >= kFirstEpiWarp && warp < kProducerWarp) {
         // unit block scales (ue8m0 127) for every MMA: whole SF region, all lanes
         const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         // half); completion is counted on the leader's barrier, which expects both
                         producer_wait(a, &u_empty[ru.idx], ru.phase ^ 1);
                         if (ptx::elect_one()) {
-                            if (a.debug_flags & 4) {  // timing experiment: no operand traffic
+                            if (experiment(a, 4)) {  // timing experiment: no operand traffic
                                 if (leader) ptx::mbar_arrive(&u_full[ru.idx]);
                             } else {
                                 if (leader) ptx::mbar_expect_tx(&u_full[ru.idx], 2 * HB);
@@ -554,21 +554,21 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             for (int64_t t = t_begin; t < t_end; ++t, ++local) {
                 const int acc = local % kAccBufs;
                 const uint32_t use = (uint32_t)(local / kAccBufs) & 1u;  // parity of this buffer's use
-                const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
-                if (tr) a.trace[local * kTrSlots + kTrMmaWait] = clock64();
+                const bool tr = trace_buf(a) && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
+                if (tr) trace_buf(a)[local * kTrSlots + kTrMmaWait] = clock64();
                 // spinning waits: the MMA warp's wake-up latency is on the critical path
                 ptx::mbar_wait(&t_empty[acc], use ^ 1);
-                if (tr) a.trace[local * kTrSlots + kTrMmaGo] = clock64();
+                if (tr) trace_buf(a)[local * kTrSlots + kTrMmaGo] = clock64();
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 for (int ks = 0; ks < n_kst; ++ks, ru.next()) {
                     const int s = ru.idx;
                     const int sa = ra.idx;
                     if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
-                    const bool trs = tr && (a.debug_flags & 8) && ks < 16;
-                    if (trs) a.trace[local * kTrSlots + kTrB0Loaded + ks] = clock64();
+                    const bool trs = tr && experiment(a, 8) && ks < 16;
+                    if (trs) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ks] = clock64();
                     ptx::mbar_wait(&u_full[s], ru.phase);
-                    if (trs) a.trace[local * kTrSlots + kTrB0Done + ks] = clock64();
+                    if (trs) trace_buf(a)[local * kTrSlots + kTrB0Done + ks] = clock64();
                     ptx::tc_fence_after();
                     // descriptors of this stage's first K-step; later steps add fixed strides
                     const uint32_t a_off = SA ? (uint32_t)(sa * AB) : (uint32_t)(ks * kWordsPerStage * CPW) * (kM * 16);
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
                 }
                 __syncwarp();
-                if (tr) a.trace[local * kTrSlots + kTrMmaIssued] = clock64();
+                if (tr) trace_buf(a)[local * kTrSlots + kTrMmaIssued] = clock64();
             }
             }
         }
@@ -762,12 +762,12 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             const int acc = local % kAccBufs;
             // the shared bound is read before the wait so its latency hides behind it
             const uint32_t shared_bound = share ? __ldcg(a.bound + q) : 0xFFFFFFFFu;
-            if (a.debug_flags & 4096)
+            if (experiment(a, 4096))
                 ptx::mbar_wait(&t_full[acc], (uint32_t)(local / kAccBufs) & 1u);
             else
                 ptx::mbar_wait_sleep(&t_full[acc], (uint32_t)(local / kAccBufs) & 1u);
-            const bool tr = a.trace && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
-            if (tr) a.trace[local * kTrSlots + kTrEpi0 + ew] = clock64();
+            const bool tr = trace_buf(a) && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
+            if (tr) trace_buf(a)[local * kTrSlots + kTrEpi0 + ew] = clock64();
             if (pub_min && (local & (local - 1)) == 0 || (pub_min && (local & 255) == 0)) {
                 const uint32_t kb = kth_smallest_published<KP>(a.list_min + (int64_t)q * kMinSlots, a.k);
                 if (kb != 0xFFFFFFFFu) {
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 const uint32_t mn = min32(v);
                 if (MODE == kTopK) {
-                    if (mn < thr_eff && !(a.debug_flags & 16)) {
+                    if (mn < thr_eff && !experiment(a, 16)) {
                         uint32_t cand = 0;
 #pragma unroll
                         for (int c = 0; c < kBatch; ++c) cand |= (v[c] < thr_eff ? 1u : 0u) << c;
@@ -814,8 +814,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                                 const bool new_best = vc < top.s[0];
                                 top.insert_last(vc, (uint32_t)(rc + c));  // raw bits; rows ascend
                                 if (pub_min && new_best) __stcg(a.list_min + (int64_t)q * kMinSlots + list_id, vc);
-                                if ((a.debug_flags & 32) && a.trace && local < a.trace_tiles)  // insertion census
-                                    atomicAdd((unsigned long long*)&a.trace[(int64_t)a.trace_tiles * kTrSlots + local], 1ull);
+                                if (experiment(a, 32) && trace_buf(a) && local < a.trace_tiles)  // insertion census
+                                    atomicAdd((unsigned long long*)&trace_buf(a)[(int64_t)a.trace_tiles * kTrSlots + local], 1ull);
                                 const uint32_t kth = top.s[KP - 1];
                                 thr_bits = kth < cap_bits ? kth : cap_bits;
                                 if (thr_bits < thr_eff) thr_eff = thr_bits;
@@ -848,14 +848,14 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 } else {
                     ptx::mbar_arrive(&t_empty[acc]);
                 }
-                if (tr) a.trace[local * kTrSlots + kTrRel0 + ew] = clock64();
+                if (tr) trace_buf(a)[local * kTrSlots + kTrRel0 + ew] = clock64();
             };
             const uint32_t ta0 = lane_base + col_base;
             if constexpr (kPreload) {
                 // every column of this warp's split in one round of loads, one wait,
                 // the accumulator released at once, then the compare work
                 uint32_t v[kPreBatches][kBatch];
-                if (!(a.debug_flags & 1)) {
+                if (!experiment(a, 1)) {
 #pragma unroll
                     for (int b = 0; b < kPreBatches; ++b) {
                         const int nb = kCols - b * kBatch < kBatch ? kCols - b * kBatch : kBatch;
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
 #pragma unroll
                         for (int c = 0; c < kBatch; ++c) v[b][c] = 0xFFFFFFFFu;
                 }
-                if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
+                if (tr && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 release();
                 if (PAIR && MODE == kFull && a.tma_out == 2) {
                     // full matrix, wide: the 4 lane-quadrant warps of this column split fill
@@ -931,15 +931,15 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     const int nb = kCols - b * kBatch < kBatch ? kCols - b * kBatch : kBatch;
                     process(v[b], b * kBatch, nb);
                 }
-                if (tr && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
+                if (tr && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Done + ew] = clock64();
                 continue;
             } else {
 #pragma unroll
             for (int b0 = 0; b0 < kCols; b0 += kBatch) {
-                if (tr && b0 == kBatch && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Done + ew] = clock64();
+                if (tr && b0 == kBatch && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Done + ew] = clock64();
                 const int nb = kCols - b0 < kBatch ? kCols - b0 : kBatch;  // multiple of 8, warp-uniform
                 uint32_t v[kBatch];
-                if (!(a.debug_flags & 1)) {
+                if (!experiment(a, 1)) {
                     // widest loads that fit (x32 moves ~40% more TMEM bytes/clk than x8)
                     const uint32_t ta = ta0 + (uint32_t)b0;
                     if (nb == 32) {
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < kBatch; ++c) v[c] = 0xFFFFFFFFu;
                 }
-                if (tr && b0 == 0 && !(a.debug_flags & 8)) a.trace[local * kTrSlots + kTrB0Loaded + ew] = clock64();
+                if (tr && b0 == 0 && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 if (b0 + kBatch >= kCols) release();
                 process(v, b0, nb);
             }
@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         }
     }
 
-    if (cta_trace) a.trace[blockIdx.x * 4 + 2] = (long long)ptx::globaltimer();
+    if (cta_trace) trace_buf(a)[blockIdx.x * 4 + 2] = (long long)ptx::globaltimer();
     ptx::tc_fence_before();
     if (PAIR)
         ptx::cluster_sync();  // the leader's MMAs and the peer's remote arrivals are all done
@@ -1001,14 +1001,30 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         else
             ptx::tmem_dealloc(tmem, Fmt<F>::kTmemCols);
     }
-    if (cta_trace) a.trace[blockIdx.x * 4 + 3] = (long long)ptx::globaltimer();
+    if (cta_trace) trace_buf(a)[blockIdx.x * 4 + 3] = (long long)ptx::globaltimer();
 }
 
 // ---- host side -------------------------------------------------------------
 
+// One mutex per (device, stream), held by launch_one_impl from scratch
+// acquisition until every kernel of the launch is enqueued.  Two host threads
+// sharing a stream (torch's default stream, say; ctypes drops the GIL) then
+// enqueue whole launches one after the other, so stream order keeps one
+// launch's streamed-A operand, progress counters and side-stream fork/join
+// from being overwritten or freed under the other's kernels.
+std::mutex& stream_mutex(cudaStream_t stream) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, std::mutex> locks;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    return locks[std::make_pair(dev, stream)];  // std::map nodes never move
+}
+
 // Launch scratch (pair progress counters, streamed-A operand) kept per
 // (device, stream) and grown on demand: stream-ordered reuse needs no
 // per-launch cudaMallocAsync, which costs ~250 us when the pool trims.
+// Callers hold stream_mutex(stream).
 void* launch_scratch(int which, size_t bytes, cudaStream_t stream) {
     static std::mutex mu;
     static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> cache;
@@ -1090,17 +1106,6 @@ int make_known_map(CUtensorMap* map, const CompareArgs& a, int box_rows) {
     return FASTID_OK;
 }
 
-int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
-
 // Spare CTA pairs left over by (unknown groups x slices) on this GPU: each
 // takes the tail tiles of groups / n_spare groups.  With S slices, a spare
 // handles `per` groups: equal run times need tail = tiles / (1 + S * per).
@@ -1125,13 +1130,13 @@ inline SparePlan spare_plan(int64_t n_tiles, int64_t groups, int slices, bool di
 
 // The spare grid assumes the SMs the regular grid leaves free are idle; on a
 // GPU shared with other work it could start late and lengthen the step, so
-// FASTID_NO_SPARE_PAIRS=1 (or debug flag 1024) turns it off.
+// FASTID_NO_SPARE_PAIRS=1 (or the database option FASTID_OPT_NO_SPARE_PAIRS) turns it off.
 inline bool spares_disabled(const CompareArgs& a) {
     static const bool env = [] {
         const char* e = getenv("FASTID_NO_SPARE_PAIRS");
         return e && *e && *e != '0';
     }();
-    return env || (a.debug_flags & 1024);
+    return env || (a.options & FASTID_OPT_NO_SPARE_PAIRS);
 }
 
 template <int F>
@@ -1237,7 +1242,8 @@ int make_a_map(CUtensorMap* map, const void* a_global, int64_t groups, int n_kst
 
 template <int F, int MODE, int KP, bool SA, bool IMG, bool PAIR>
 int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) {
-    HostClock hc(a_in.debug_flags & 128);
+    HostClock hc(experiment(a_in, 128));
+    std::lock_guard<std::mutex> launch_lock(stream_mutex(stream));
     CompareArgs a = a_in;
     CUtensorMap omap;
     memset(&omap, 0, sizeof(omap));
@@ -1247,9 +1253,9 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     // only when every granule they touch belongs to the matrix: n_queries % 4 == 0
     if (PAIR && MODE == kFull && a.n_queries > 0 && a.n_queries % 4 == 0 && ((uintptr_t)a.out & 15) == 0 &&
         (a.ld_out * 4) % 16 == 0 &&
-        !(a.debug_flags & 256) && Layout<F>(a.stride, SA, IMG, PAIR, out_stage_bytes<F, MODE, IMG, PAIR>()).fits()) {
-        // wide blocks (128 unknowns = 512-B rows) unless debug flag 2048 asks for the per-warp ones
-        const bool wide = !(a.debug_flags & 2048);
+        !(a.options & FASTID_OPT_NO_TMA_STORE) && Layout<F>(a.stride, SA, IMG, PAIR, out_stage_bytes<F, MODE, IMG, PAIR>()).fits()) {
+        // wide blocks (128 unknowns = 512-B rows) unless FASTID_OPT_NARROW_TMA_STORE asks for per-warp ones
+        const bool wide = !(a.options & FASTID_OPT_NARROW_TMA_STORE);
         if (int rc = make_out_map(&omap, a, Fmt<F>::BN / (Roles<F, IMG>::kEpiWarps / 4), wide ? kM : 32)) return rc;
         a.tma_out = wide ? 2 : 1;
     }
@@ -1276,7 +1282,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         a_global = (uint8_t*)launch_scratch(0, bytes, stream);
         if (!a_global) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %zu bytes of streamed-A operand", bytes);
         const int64_t work = groups * lay.n_kst * kM;
-        prep_a_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 16), 256, 0, stream>>>(
+        prep_a_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), num_sms() * 16), 256, 0, stream>>>(
             a, (int)groups, lay.n_kst, a_global);
         FASTID_LAUNCHED("prep_a_kernel");
         if (PAIR) {
@@ -1348,7 +1354,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
 // fits (L <= 2048) and a streamed one otherwise.
 template <int F>
 bool use_pair(const CompareArgs& a) {
-    return F == FASTID_TENSOR_F4 && a.image != nullptr && !(a.debug_flags & 2) &&
+    return F == FASTID_TENSOR_F4 && a.image != nullptr && !(a.options & FASTID_OPT_NO_CTA_PAIRS) &&
            (Layout<F>(a.stride, false, true, true).fits() || Layout<F>(a.stride, true, true, true).fits());
 }
 
@@ -1434,7 +1440,7 @@ int build_image_fmt(const CompareArgs& a, void* image, cudaStream_t stream) {
     const int64_t tiles = ceil_div(a.n_refs, Fmt<F>::BN);
     const int64_t work = tiles * lay.n_kst * 2 * Fmt<F>::BN;
     if (work == 0) return FASTID_OK;
-    build_image_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 32), 256, 0, stream>>>(
+    build_image_kernel<F><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), num_sms() * 32), 256, 0, stream>>>(
         a, tiles, lay.n_kst, (uint8_t*)image);
     FASTID_LAUNCHED("build_image_kernel");
     return FASTID_OK;

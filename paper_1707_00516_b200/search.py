@@ -22,7 +22,16 @@ import torch
 from .compare import DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device
 from .panel import ThresholdHits, TopKResult
 
-__all__ = ["KnownDatabase", "PreparedImage", "QueryStager"]
+__all__ = ["KnownDatabase", "PreparedImage", "QueryStager", "DB_OPTIONS"]
+
+# Execution variants of a prepared database (fastid_db_option, include/fastid_b200.h).
+# Each computes the same result; they select among kernel paths.
+DB_OPTIONS = {
+    "no_cta_pairs": 1,       # single-CTA split-B kernel instead of CTA pairs
+    "no_tma_store": 2,       # full matrix by per-element stores
+    "no_spare_pairs": 4,     # no spare-pair grid on the SMs the regular grid leaves free
+    "narrow_tma_store": 8,   # per-warp (32-unknown) TMA-store blocks
+}
 
 
 class PreparedImage:
@@ -47,6 +56,22 @@ class PreparedImage:
                                              ctypes.byref(self.handle)), "fastid_db_create")
         self.formulation = L.fastid_db_formulation(self.handle)
         self.image_bytes = L.fastid_db_image_bytes(panel.n_profiles, panel.bit_length, self.formulation)
+
+    def set_option(self, name: str, enabled: bool = True) -> None:
+        """Switch one DB_OPTIONS execution variant on or off for later calls."""
+        from . import _native
+
+        if name not in DB_OPTIONS:
+            raise ValueError(f"option must be one of {sorted(DB_OPTIONS)}, got {name!r}")
+        _native.check(_native.lib().fastid_db_set_option(self.handle, DB_OPTIONS[name], int(bool(enabled))),
+                      "fastid_db_set_option")
+
+    @property
+    def options(self) -> set:
+        from . import _native
+
+        bits = _native.lib().fastid_db_options(self.handle)
+        return {n for n, b in DB_OPTIONS.items() if bits & b}
 
     def __del__(self):
         try:
@@ -127,6 +152,12 @@ class KnownDatabase:
                               RuntimeWarning, stacklevel=3)
         return None
 
+    def set_option(self, name: str, enabled: bool = True) -> None:
+        """Select an execution variant of the prepared image (DB_OPTIONS); every
+        variant returns the same result.  No effect without a tensor image."""
+        if self.image is not None:
+            self.image.set_option(name, enabled)
+
     @property
     def n_profiles(self) -> int:
         return self.panel.n_profiles
@@ -159,6 +190,43 @@ class KnownDatabase:
             self._stagers[key] = st
         return st
 
+    def stage_queries(self, query_words: np.ndarray, k: int, stager: QueryStager | None = None) -> QueryStager:
+        """Host (N_Q, N_W) words -> the stager's device panel, enqueued on the current
+        stream: copy into pinned staging, H2D, encode into the aligned row layout.
+        Validates the words as the reference Panel does (width, word count,
+        zero padding past L)."""
+        from . import _native
+        from .errors import CorruptProfileError, PanelMismatchError
+        from .panel import padding_mask
+
+        p = self.panel
+        qw = np.ascontiguousarray(query_words)
+        if qw.dtype.itemsize * 8 != p.word_width or qw.ndim != 2 or qw.shape[1] != p.n_words:
+            raise PanelMismatchError(f"query words {qw.shape}/{qw.dtype} do not match the database "
+                                     f"({p.n_words} x {p.word_width}-bit words)")
+        mask = padding_mask(p.bit_length, p.word_width)
+        if mask and qw.size and np.any(qw[:, -1] & qw.dtype.type(mask)):
+            raise CorruptProfileError(f"nonzero padding past bit {p.bit_length}")
+        n_q = qw.shape[0]
+        st = stager or self.stager(n_q, k)
+        st.host_in.numpy()[:] = qw.view(np.uint8).reshape(n_q, -1)
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            st.dev_in.copy_(st.host_in, non_blocking=True)
+            _native.check(_native.lib().fastid_load_words(
+                st.dev_in.data_ptr(), n_q, st.dev_in.shape[1], st.panel.rows.data_ptr(), st.panel.stride,
+                stream.cuda_stream), "fastid_load_words")
+        return st
+
+    def fetch_lists(self, st: QueryStager, s: torch.Tensor, x: torch.Tensor) -> tuple[np.ndarray, np.ndarray]:
+        """D2H of a (scores, index) result through the stager's pinned buffers."""
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            st.host_s.copy_(s, non_blocking=True)
+            st.host_x.copy_(x, non_blocking=True)
+            stream.synchronize()
+        return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
+
     def search_words(self, query_words: np.ndarray, k: int = 16, max_score: int | None = None,
                      stager: QueryStager | None = None) -> tuple[np.ndarray, np.ndarray]:
         """Top-k of a (N_Q, N_W) host word array -> host (scores u32 [N_Q,k], index i64 [N_Q,k]).
@@ -166,29 +234,10 @@ class KnownDatabase:
         Per call: pinned H2D of the unknowns, on-device encode into the row
         layout, fused compare + top-k, D2H of the (score, index) lists.
         """
-        p = self.panel
-        qw = np.ascontiguousarray(query_words)
-        if qw.dtype.itemsize * 8 != p.word_width or qw.ndim != 2 or qw.shape[1] != p.n_words:
-            from .errors import PanelMismatchError
-
-            raise PanelMismatchError(f"query words {qw.shape}/{qw.dtype} do not match the database "
-                                     f"({p.n_words} x {p.word_width}-bit words)")
-        n_q = qw.shape[0]
-        st = stager or self.stager(n_q, k)
-        st.host_in.numpy()[:] = qw.view(np.uint8).reshape(n_q, -1)
-        stream = torch.cuda.current_stream(self.device)
+        st = self.stage_queries(query_words, k, stager)
         with torch.cuda.device(self.device):
-            st.dev_in.copy_(st.host_in, non_blocking=True)
-            from . import _native
-
-            _native.check(_native.lib().fastid_load_words(
-                st.dev_in.data_ptr(), n_q, st.dev_in.shape[1], st.panel.rows.data_ptr(), st.panel.stride,
-                stream.cuda_stream), "fastid_load_words")
             s, x = self.topk_device(st.panel, k, max_score, st.workspace, (st.out_s, st.out_x))
-            st.host_s.copy_(s, non_blocking=True)
-            st.host_x.copy_(x, non_blocking=True)
-            stream.synchronize()
-        return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
+        return self.fetch_lists(st, s, x)
 
     def search(self, queries, k: int = 16, max_score: int | None = None) -> TopKResult:
         """Per unknown, the k closest knowns by (score asc, global index asc)."""

@@ -8,7 +8,9 @@ independent, so the only exchange is the final one the north star names: an
 all-gather of each rank's fixed-size top-k candidate lists (N_Q x k x
 (4 + 8) bytes per rank, NCCL over NVLink), followed by the same
 (score, index) merge kernel the single-GPU path uses.  Threshold hits add a
-count exchange, then a variable-size gather.
+count exchange, then a gather padded to the largest count
+(``gather_hits`` / ``ShardedDatabase.threshold``); the union is ordered by
+(unknown, known) like the single-GPU result.
 
 No reference implementation exists for this layer (SPEC.md:15, 280;
 PAPER.md:197 lists multi-GPU as future work).
@@ -24,7 +26,7 @@ import torch.distributed as dist
 
 from . import _native
 
-__all__ = ["shard_range", "gather_candidates", "merge_candidates", "ShardedDatabase"]
+__all__ = ["shard_range", "gather_candidates", "merge_candidates", "gather_hits", "ShardedDatabase"]
 
 
 def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
@@ -48,6 +50,48 @@ def gather_candidates(scores: torch.Tensor, index: torch.Tensor, group=None):
         dist.all_gather(list(s_all.unbind(0)), scores.contiguous(), group=group)
         dist.all_gather(list(x_all.unbind(0)), index.contiguous(), group=group)
     return s_all, x_all
+
+
+def gather_hits(query: np.ndarray, ref: np.ndarray, score: np.ndarray, group=None, device=None):
+    """Variable-size gather of every rank's threshold hits -> the union on every rank,
+    ordered by (unknown, known index).
+
+    Step 1 all-gathers the per-rank hit counts; step 2 all-gathers the hit
+    triples padded to the largest count (fixed-size collectives, so NCCL's
+    all_gather_into_tensor applies); the padding is dropped on receipt.  Rows are
+    disjoint between ranks, so no (unknown, known) pair appears twice.
+    ``device`` holds the collective buffers (a CUDA device for NCCL, None = CPU).
+    """
+    world = dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    n = int(query.shape[0])
+    counts = torch.zeros((world, 1), dtype=torch.int64, device=dev)
+    mine = torch.tensor([n], dtype=torch.int64, device=dev)
+    if nccl:
+        dist.all_gather_into_tensor(counts, mine, group=group)
+    else:
+        dist.all_gather(list(counts.unbind(0)), mine, group=group)
+    counts = counts.cpu().numpy()[:, 0]
+    m = int(counts.max()) if world else 0
+    if m == 0:
+        return (np.zeros(0, np.uint32), np.zeros(0, np.int64), np.zeros(0, np.uint32))
+    # one (m, 3) int64 block per rank: unknown, known, score
+    block = torch.full((m, 3), -1, dtype=torch.int64, device=dev)
+    if n:
+        block[:n, 0] = torch.from_numpy(query.astype(np.int64))
+        block[:n, 1] = torch.from_numpy(ref.astype(np.int64))
+        block[:n, 2] = torch.from_numpy(score.astype(np.int64))
+    every = torch.empty((world, m, 3), dtype=torch.int64, device=dev)
+    if nccl:
+        dist.all_gather_into_tensor(every, block, group=group)
+    else:
+        dist.all_gather(list(every.unbind(0)), block, group=group)
+    every = every.cpu().numpy()
+    rows = np.concatenate([every[r, : counts[r]] for r in range(world)])
+    order = np.lexsort((rows[:, 1], rows[:, 0]))
+    rows = rows[order]
+    return rows[:, 0].astype(np.uint32), rows[:, 1].astype(np.int64), rows[:, 2].astype(np.uint32)
 
 
 def merge_candidates(s_all: torch.Tensor, x_all: torch.Tensor, k: int, out=None):
@@ -91,6 +135,21 @@ class ShardedDatabase:
         s_all, x_all = gather_candidates(s, x, self.group)
         return self.merge(s_all, x_all, k)
 
+    def threshold(self, queries, threshold: int, capacity: int | None = None):
+        """Every (unknown j, global known i, score) with score <= threshold over the
+        whole sharded database, ordered by (j, i), on every rank: the local
+        threshold epilogue, then gather_hits."""
+        from .panel import ThresholdHits
+
+        hits = self.local.threshold(queries, threshold, capacity)
+        if self.world == 1:
+            return hits
+        dev = getattr(self.local, "device", None)
+        if dev is not None and dist.get_backend(self.group) != "nccl":
+            dev = None
+        q, r, sc = gather_hits(hits.query, hits.ref, hits.score, self.group, dev)
+        return ThresholdHits(q, r, sc, int(threshold))
+
     def topk_device(self, queries, k: int, max_score: int | None = None, workspace=None, out=None):
         s, x = self.local.topk_device(queries, k, max_score, workspace, out)
         return self.combine(s, x, k)
@@ -98,18 +157,7 @@ class ShardedDatabase:
     def search_words(self, query_words: np.ndarray, k: int = 16, max_score: int | None = None):
         """Host unknowns -> global top-k (host arrays) on every rank."""
         db = self.local
-        n_q = query_words.shape[0]
-        st = db.stager(n_q, k)
-        qw = np.ascontiguousarray(query_words)
-        st.host_in.numpy()[:] = qw.view(np.uint8).reshape(n_q, -1)
-        stream = torch.cuda.current_stream(db.device)
+        st = db.stage_queries(query_words, k)
         with torch.cuda.device(db.device):
-            st.dev_in.copy_(st.host_in, non_blocking=True)
-            _native.check(_native.lib().fastid_load_words(
-                st.dev_in.data_ptr(), n_q, st.dev_in.shape[1], st.panel.rows.data_ptr(), st.panel.stride,
-                stream.cuda_stream), "fastid_load_words")
             s, x = self.topk_device(st.panel, k, max_score, st.workspace, (st.out_s, st.out_x))
-            st.host_s.copy_(s, non_blocking=True)
-            st.host_x.copy_(x, non_blocking=True)
-            stream.synchronize()
-        return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
+        return db.fetch_lists(st, s, x)

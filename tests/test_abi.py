@@ -66,3 +66,19 @@ def test_sass_uses_blackwell_features():
     assert "UTMALDG" in sass
     assert "LDTM" in sass
     assert "POPC" in sass
+
+
+def test_experiment_switches_only_in_the_diag_build():
+    """The product library neither declares nor exports the process-global timing
+    switches (result-invalidating by design); they live in the experiments build."""
+    header = (_native.INCLUDE / "fastid_b200.h").read_text()
+    assert "fastid_debug_flags" not in header and "fastid_debug_trace" not in header
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "fastid_debug" not in out
+    assert "fastid_db_set_option" in out
+    diag = (_native.INCLUDE / "fastid_b200_diag.h").read_text()
+    assert "fastid_debug_flags" in diag
+    if _native.DIAG_LIB_PATH.exists():
+        out = subprocess.run(["nm", "-D", "--defined-only", str(_native.DIAG_LIB_PATH)], capture_output=True,
+                             text=True).stdout
+        assert "fastid_debug_flags" in out and "fastid_debug_trace" in out

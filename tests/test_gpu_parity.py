@@ -306,7 +306,7 @@ def test_prepared_database_image(rng, form, L):
                                    (3001, 388, 1024), (5000, 260, 512), (1500, 300, 5000), (900, 520, 2304)])
 def test_image_pairs_and_split(rng, pairs, shape):
     """Prepared mxf4 image: the CTA-pair kernel (cta_group::2, M=256) and the
-    single-CTA split-B kernel (debug flag 2) both equal the oracle, for every
+    single-CTA split-B kernel (option no_cta_pairs) both equal the oracle, for every
     epilogue, with ragged unknown groups and known tiles.  Unknown counts that
     are multiples of 4 with L <= 1024 take the TMA-store full-matrix epilogue,
     the others its direct-store fallback."""
@@ -320,26 +320,22 @@ def test_image_pairs_and_split(rng, pairs, shape):
     q, _ = rand_words(rng, n_q, nw, 64, L)
     q[: n_q // 4] = r[rng.integers(0, n_r, n_q // 4)]
     r[n_r // 2 : n_r // 2 + 3] = r[:3]
-    lib = _native.lib()
-    lib.fastid_debug_flags(0 if pairs else 2)
-    try:
-        db = KnownDatabase(r, L, formulation="tensor_f4", ref_base=7)
-        dq = m.DevicePanel.from_words(q, L)
-        exp = oracle.naive(r, q)
-        full = db.full_device(dq).cpu().numpy().view(np.uint32)
-        assert np.array_equal(full, exp)
-        for k in (1, 16, 32):
-            s, x = db.search_words(q, k)
-            es, ex, _ = oracle.topk_from_matrix(exp, k)
-            assert np.array_equal(s, es), k
-            assert np.array_equal(x, np.where(ex >= 0, ex + 7, -1)), k
-        thr = int(np.percentile(exp, 2))
-        hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
-        hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
-        assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 7)
-        assert np.array_equal(hits.score, hs)
-    finally:
-        lib.fastid_debug_flags(0)
+    db = KnownDatabase(r, L, formulation="tensor_f4", ref_base=7)
+    db.set_option("no_cta_pairs", not pairs)
+    dq = m.DevicePanel.from_words(q, L)
+    exp = oracle.naive(r, q)
+    full = db.full_device(dq).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, exp)
+    for k in (1, 16, 32):
+        s, x = db.search_words(q, k)
+        es, ex, _ = oracle.topk_from_matrix(exp, k)
+        assert np.array_equal(s, es), k
+        assert np.array_equal(x, np.where(ex >= 0, ex + 7, -1)), k
+    thr = int(np.percentile(exp, 2))
+    hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
+    hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
+    assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 7)
+    assert np.array_equal(hits.score, hs)
 
 
 @pytest.mark.parametrize("k,max_score", [(5, None), (16, 240), (1, 250), (32, None)])
@@ -406,7 +402,7 @@ def test_pairs_large_panels(rng, shape):
     drift control active, and -- where (unknown groups x slices) leaves SMs
     free -- the spare-pair grid over the tail tiles of several groups): top-k,
     threshold and full rows near both ends of the known range equal the oracle,
-    and the top-k equals the launch without spare pairs (debug flag 1024)."""
+    and the top-k equals the launch without spare pairs (option no_spare_pairs)."""
     import torch
 
     m = fb()
@@ -422,14 +418,9 @@ def test_pairs_large_panels(rng, shape):
     pick = np.arange(0, n_q, 7)
     es, ex, _ = oracle.topk(r, q[pick], 16)
     assert np.array_equal(s[pick], es) and np.array_equal(x[pick], ex)
-    from paper_1707_00516_b200 import _native
-
-    lib = _native.lib()
-    lib.fastid_debug_flags(1024)
-    try:
-        s2, x2 = db.search_words(q, 16)
-    finally:
-        lib.fastid_debug_flags(0)
+    db.set_option("no_spare_pairs")
+    s2, x2 = db.search_words(q, 16)
+    db.set_option("no_spare_pairs", False)
     assert np.array_equal(s, s2) and np.array_equal(x, x2)
     dq = m.DevicePanel.from_words(q, L)
     full = db.full_device(dq)
@@ -489,7 +480,7 @@ def test_full_matrix_writes_stay_in_view(rng, n_r, n_q):
     """The full matrix is written into a poisoned view [n_r, n_q] of a larger buffer
     (row pitch 160, 100 extra rows): every cell outside the view keeps the poison,
     for every formulation, with and without the prepared image and for each epilogue
-    store variant (debug flags 256: no TMA store, 2048: per-warp TMA blocks). Covers
+    store variant (options no_tma_store / narrow_tma_store). Covers
     the TMA unit's 16-byte clipping of partial unknown granules."""
     m = fb()
     from paper_1707_00516_b200 import _native
@@ -501,24 +492,22 @@ def test_full_matrix_writes_stay_in_view(rng, n_r, n_q):
     exp = oracle.naive(r, q)
     dq = m.DevicePanel.from_words(q, L)
     dr = m.DevicePanel.from_words(r, L)
-    try:
-        for form in ("tensor_f4", "tensor_i8", "popc"):
-            db = KnownDatabase(r, L, formulation=form)
-            for flags in (0, 256, 2048):
-                _native.lib().fastid_debug_flags(flags)
-                for use_db in (True, False):
-                    buf = torch.full((n_r + 100, 160), -1, dtype=torch.int32, device=dq.rows.device)
-                    view = buf[:n_r, :n_q]
-                    if use_db:
-                        db.full_device(dq, view)
-                    else:
-                        m.compare.compare_device(dr, dq, view, form)
-                    g = buf.cpu().numpy().view(np.uint32)
-                    assert np.array_equal(g[:n_r, :n_q], exp), (form, flags, use_db)
-                    g[:n_r, :n_q] = 0xFFFFFFFF
-                    assert (g == 0xFFFFFFFF).all(), (form, flags, use_db, "write outside the view")
-    finally:
-        _native.lib().fastid_debug_flags(0)
+    for form in ("tensor_f4", "tensor_i8", "popc"):
+        db = KnownDatabase(r, L, formulation=form)
+        for flags in ((), ("no_tma_store",), ("narrow_tma_store",)):
+            for name in ("no_tma_store", "narrow_tma_store"):
+                db.set_option(name, name in flags)
+            for use_db in (True, False):
+                buf = torch.full((n_r + 100, 160), -1, dtype=torch.int32, device=dq.rows.device)
+                view = buf[:n_r, :n_q]
+                if use_db:
+                    db.full_device(dq, view)
+                else:
+                    m.compare.compare_device(dr, dq, view, form)
+                g = buf.cpu().numpy().view(np.uint32)
+                assert np.array_equal(g[:n_r, :n_q], exp), (form, flags, use_db)
+                g[:n_r, :n_q] = 0xFFFFFFFF
+                assert (g == 0xFFFFFFFF).all(), (form, flags, use_db, "write outside the view")
 
 
 @pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8", "popc"])

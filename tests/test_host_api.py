@@ -102,3 +102,25 @@ def test_cli_exit_codes(tmp_path):
         main(["compare", "--refs", "a"])
     assert info.value.code == 2
     assert main(["compare", "--refs", str(tmp_path / "nope"), "--queries", "q", "--out", "o"]) == 1
+
+
+def test_device_panel_validates_words_before_device_work():
+    """DevicePanel.from_words (behind KnownDatabase(raw_words, L)) applies the
+    reference Panel's rules on the host before touching a device: wrong word
+    counts raise ValueError, nonzero padding CorruptProfileError."""
+    with pytest.raises(ValueError):
+        fb.DevicePanel.from_words(np.zeros((3, 1), np.uint64), 100)  # needs 2 words
+    with pytest.raises(ValueError):
+        fb.DevicePanel.from_words(np.zeros((3, 3), np.uint32), 64)   # needs 2 words
+    bad = np.zeros((2, 2), np.uint64)
+    bad[1, 1] = 1  # bit 127 set, L = 100
+    with pytest.raises(fb.CorruptProfileError):
+        fb.DevicePanel.from_words(bad, 100)
+    with pytest.raises(ValueError):
+        fb.DevicePanel.from_words(np.zeros((2, 2), np.uint64), 0)
+
+
+def test_known_database_options_are_named():
+    from paper_1707_00516_b200.search import DB_OPTIONS
+
+    assert DB_OPTIONS == {"no_cta_pairs": 1, "no_tma_store": 2, "no_spare_pairs": 4, "narrow_tma_store": 8}

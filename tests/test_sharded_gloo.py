@@ -36,6 +36,13 @@ class OracleShard:
         self.refs = refs
         self.start = start
 
+    def threshold(self, queries, t, capacity=None):
+        import oracle
+        from paper_1707_00516_b200.panel import ThresholdHits
+
+        q, r, sc, _ = oracle.threshold(self.refs, queries, t)
+        return ThresholdHits(q, r + self.start, sc, t)
+
     def topk_device(self, queries, k, max_score=None, workspace=None, out=None):
         import oracle
 
@@ -87,6 +94,51 @@ def test_sharded_topk_matches_single_shard(world):
     assert all(p.exitcode == 0 for p in procs)
     ok_s, ok_x = q.get(timeout=5)
     assert ok_s and ok_x
+
+
+def _threshold_worker(rank, world, port, n_total, n_q, L, result_q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_1707_00516_b200.sharded import ShardedDatabase, shard_range
+
+    rng = np.random.default_rng(7)
+    refs = rng.integers(0, 2**64, (n_total, L // 64), dtype=np.uint64)
+    # copies of rows of the first quarter only: at t = 0 the other ranks have no hits
+    queries = refs[rng.integers(0, n_total // 4, n_q)].copy()
+    queries[::3, 0] ^= np.uint64(0xFF)
+    refs[n_total - 5] = refs[2]  # the same profile in the first and the last shard
+    start, stop = shard_range(n_total, rank, world)
+    db = ShardedDatabase(OracleShard(refs[start:stop], start), n_total)
+    for t in (0, 8, L // 4, 0):
+        hits = db.threshold(queries, t)
+        if rank == 0:
+            eq, er, es, _ = oracle.threshold(refs, queries, t)
+            result_q.put((t, np.array_equal(hits.query, eq) and np.array_equal(hits.ref, er)
+                          and np.array_equal(hits.score, es), len(hits)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_threshold_matches_single_shard(world):
+    """Threshold hits of every rank: count all-gather, padded all-gather, (j, i)
+    order -- equal to the single-shard oracle, including a threshold (t = 0) at
+    which only the first rank has hits."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_threshold_worker, args=(r, world, port, 997, 29, 256, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    for _ in range(4):
+        t, ok, n = q.get(timeout=5)
+        assert ok, (t, n)
 
 
 def test_merge_lists_oracle():

@@ -3,7 +3,8 @@ cuda:0, candidates all-gathered over gloo (a one-GPU box has no second device
 for NCCL; the NCCL path differs only in the transport).  Each rank's
 KnownDatabase (prepared image, CTA-pair kernel) searches its contiguous shard
 with global indices; the gathered-and-merged top-k must equal the oracle's
-top-k over the whole panel on every rank, including cross-shard ties."""
+top-k over the whole panel on every rank, including cross-shard ties, and the
+gathered threshold hits must equal the oracle's hit list."""
 
 import os
 import socket
@@ -38,7 +39,10 @@ def _worker(rank, world, port, refs, queries, L, k, result_q):
     start, stop = shard_range(len(refs), rank, world)
     db = ShardedDatabase(KnownDatabase(refs[start:stop], L, ref_base=start, formulation="tensor_f4"), len(refs))
     s, x = db.search_words(queries, k)
-    result_q.put((rank, s, x))
+    from paper_1707_00516_b200.panel import Panel
+
+    hits = db.threshold(Panel(tuple(range(len(queries))), queries, L), L // 8)
+    result_q.put((rank, s, x, hits.query, hits.ref, hits.score))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -66,6 +70,10 @@ def test_sharded_two_ranks_real_kernels(rng):
         p.join(timeout=60)
         assert p.exitcode == 0
     es, ex, _ = oracle.topk(refs, queries, k)
-    for rank, s, x in out:
+    hq, hr, hs, _ = oracle.threshold(refs, queries, L // 8)
+    assert len(hq) >= 52
+    for rank, s, x, tq, tr, ts in out:
         assert np.array_equal(s, es) and np.array_equal(x, ex), rank
+        # threshold hits of both shards: count exchange + padded gather, (j, i) order
+        assert np.array_equal(tq, hq) and np.array_equal(tr, hr) and np.array_equal(ts, hs), rank
     assert 7 in ex[50] and n_r // 2 + 5 in ex[50]

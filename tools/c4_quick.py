@@ -9,7 +9,7 @@ from paper_1707_00516_b200.search import KnownDatabase
 n_r, n_q, L = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (5_000_000, 512, 5000)))
 import os
 from paper_1707_00516_b200 import _native
-_native.lib().fastid_debug_flags(int(os.environ.get("FASTID_FLAGS", "0")))
+_native.diag_lib().fastid_debug_flags(int(os.environ.get("FASTID_FLAGS", "0")))
 g = torch.Generator(device="cuda").manual_seed(0)
 nw = -(-L // 64)
 r = torch.randint(-(2**63), 2**63 - 1, (n_r, nw), dtype=torch.int64, device="cuda", generator=g)

@@ -17,7 +17,7 @@ g = torch.Generator(device="cuda").manual_seed(0)
 r = torch.randint(-(2**63), 2**63 - 1, (n_r, L // 64), dtype=torch.int64, device="cuda", generator=g)
 src = torch.randint(0, n_r, (n_q,), device="cuda", generator=g)
 q = r[src].clone()
-lib = _native.lib()
+lib = _native.diag_lib()
 dq = m.DevicePanel.from_words(q, L)
 panel = m.DevicePanel.from_words(r, L)
 del r

@@ -15,7 +15,7 @@ q = r[torch.randint(0, n_r, (n_q,), device="cuda", generator=g)].clone()
 db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation="tensor_f4")
 del r
 dq = m.DevicePanel.from_words(q, L)
-lib = _native.lib()
+lib = _native.diag_lib()
 for _ in range(3):
     db.topk_device(dq, 16)
 torch.cuda.synchronize()

@@ -16,7 +16,7 @@ db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation="tensor_f4")
 del r
 dq = m.DevicePanel.from_words(q, L)
 ws = torch.empty(m.compare.topk_workspace_bytes(n_r, n_q, 16, "tensor_f4"), dtype=torch.uint8, device="cuda")
-lib = _native.lib()
+lib = _native.diag_lib()
 FLAG = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 res = {0: [], FLAG: []}
 for rd in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):

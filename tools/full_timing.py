@@ -16,7 +16,7 @@ g = torch.Generator(device="cuda").manual_seed(0)
 nw = L // 64
 rw = torch.randint(-2**62, 2**62, (n_r, nw), dtype=torch.int64, device="cuda", generator=g)
 qw = torch.randint(-2**62, 2**62, (n_q, nw), dtype=torch.int64, device="cuda", generator=g)
-lib = _native.lib()
+lib = _native.diag_lib()
 import os
 lib.fastid_debug_flags(int(os.environ.get("FASTID_FLAGS", "0")))
 for form in (os.environ.get("FASTID_FORMS", "tensor_f4,tensor_i8")).split(","):

@@ -13,7 +13,7 @@ dq = m.DevicePanel.from_words(q, L)
 ws = torch.empty(m.compare.topk_workspace_bytes(n_r, n_q, 16, "tensor_f4"), dtype=torch.uint8, device="cuda")
 out = (torch.empty((n_q, 16), dtype=torch.int32, device="cuda"), torch.empty((n_q, 16), dtype=torch.int64, device="cuda"))
 db.topk_device(dq, 16, None, ws, out); torch.cuda.synchronize()
-lib = _native.lib()
+lib = _native.diag_lib()
 lib.fastid_debug_flags(128)
 for i in range(3):
     h0 = time.perf_counter()

@@ -19,7 +19,7 @@ qw = torch.randint(-2**62, 2**62, (n_q, nw), dtype=torch.int64, device="cuda", g
 db = KnownDatabase(m.DevicePanel.from_words(rw, L), formulation="tensor_f4")
 dq = m.DevicePanel.from_words(qw, L)
 del rw
-lib = _native.lib()
+lib = _native.diag_lib()
 for flags, name in ((0, "pair"), (2, "single"), (1, "pair-noepi"), (4, "pair-noload")):
     lib.fastid_debug_flags(flags)
     out = db.topk_device(dq, 16)

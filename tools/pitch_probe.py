@@ -23,7 +23,7 @@ for L in (300, 1024):
         for form in ("tensor_f4", "tensor_i8", "popc"):
             for img in (True, False):
                 for flags in (0, 256, 2048):
-                    _native.lib().fastid_debug_flags(flags)
+                    _native.diag_lib().fastid_debug_flags(flags)
                     buf = torch.full((n_r + 100, 160), -1, dtype=torch.int32, device="cuda")
                     p = buf[:n_r, :n_q]
                     if img:
@@ -39,5 +39,5 @@ for L in (300, 1024):
                         bad_any = True
                         print(L, n_r, n_q, form, "image" if img else "plain", flags, "MISMATCH" if not ok else "ok",
                               "clobbered cols", bad_cols[:8], "rows", bad_rows)
-_native.lib().fastid_debug_flags(0)
+_native.diag_lib().fastid_debug_flags(0)
 print("pitch probe:", "FAIL" if bad_any else "all writes inside the view")

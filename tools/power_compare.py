@@ -8,7 +8,7 @@ import paper_1707_00516_b200 as m
 from paper_1707_00516_b200 import _native
 from paper_1707_00516_b200.search import KnownDatabase
 
-L = _native.lib()
+L = _native.diag_lib()
 n_r, n_q, Lc = 20_000_000, 2048, 1024
 g = torch.Generator(device="cuda").manual_seed(0)
 r = torch.randint(-(2**63), 2**63 - 1, (n_r, Lc // 64), dtype=torch.int64, device="cuda", generator=g)

@@ -17,7 +17,7 @@ q = torch.randint(-2**62, 2**62, (n_q, L // 64), dtype=torch.int64, device="cuda
 db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation="tensor_f4")
 del r
 dq = m.DevicePanel.from_words(q, L)
-lib = _native.lib()
+lib = _native.diag_lib()
 db.topk_device(dq, 16); torch.cuda.synchronize()
 buf = torch.zeros((148 * 4,), dtype=torch.int64, device="cuda")
 lib.fastid_debug_flags(64)
