@@ -69,6 +69,9 @@ FASTID_API const char* fastid_last_error(void);
 FASTID_API int64_t fastid_row_stride(int64_t bit_length);
 /* largest k accepted by fastid_compare_topk */
 FASTID_API int fastid_max_k(void);
+/* Kernels this library has enqueued so far in this process (all devices and
+ * streams): a measurement aid -- bench.py reads it around its timed region. */
+FASTID_API unsigned long long fastid_launch_count(void);
 /* 1 if `formulation` can run panels of bit_length loci on this build, else 0 */
 FASTID_API int fastid_supports(int formulation, int64_t bit_length);
 

@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_topk.restype = i32
         L.oracle_threshold.argtypes = [vp, i64, vp, i64, i64, i32, u32, i64, vp, vp, vp]
         L.oracle_threshold.restype = i64
+        L.oracle_scan.argtypes = [vp, i64, vp, i64, i64, i32, i32, u32, i32, u32, i32, vp, vp, vp, i64, vp, vp, vp]
+        L.oracle_scan.restype = i64
         L.oracle_score_word.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         L.oracle_score_word.restype = u32
         _lib = L
@@ -148,6 +150,36 @@ def threshold(refs: np.ndarray, queries: np.ndarray, t: int, capacity: int | Non
                                _ptr(hq), _ptr(hr), _ptr(hs))
     m = min(n, cap)
     return hq[:m].copy(), hr[:m].copy(), hs[:m].copy(), int(n)
+
+
+def scan(refs: np.ndarray, queries: np.ndarray, k: int = 0, max_score: int = 0xFFFFFFFF,
+         threshold: int | None = None, capacity: int = 1 << 24, workers: int | None = None):
+    """Database-scale derivations with all host threads (oracle_scan): the top-k
+    of ``topk`` (k > 0) and/or the hits of ``threshold``, over row ranges merged
+    in row order.  Returns (scores, index, counts) for k > 0 (else None) and
+    (query, ref, score, total) when ``threshold`` is given (else None)."""
+    refs, queries = _words(refs), _words(queries)
+    assert refs.dtype == queries.dtype and refs.shape[1] == queries.shape[1]
+    nq = queries.shape[0]
+    kk = max(k, 1)
+    s = np.full((nq, kk), 0xFFFFFFFF, dtype=np.uint32)
+    x = np.full((nq, kk), -1, dtype=np.int64)
+    c = np.zeros(max(nq, 1), dtype=np.int32)
+    want = threshold is not None
+    cap = capacity if want else 0
+    hq = np.zeros(max(cap, 1), dtype=np.uint32)
+    hr = np.zeros(max(cap, 1), dtype=np.int64)
+    hs = np.zeros(max(cap, 1), dtype=np.uint32)
+    n = lib().oracle_scan(_ptr(refs), refs.shape[0], _ptr(queries), nq, refs.shape[1], refs.dtype.itemsize * 8,
+                          k, max_score, int(want), int(threshold or 0), workers or os.cpu_count() or 1,
+                          _ptr(s), _ptr(x), _ptr(c), cap, _ptr(hq), _ptr(hr), _ptr(hs))
+    assert n >= 0, "oracle_scan failed"
+    top = (s, x, c[:nq]) if k > 0 else None
+    hits = None
+    if want:
+        m = min(n, cap)
+        hits = (hq[:m].copy(), hr[:m].copy(), hs[:m].copy(), int(n))
+    return top, hits
 
 
 def score_word(r: int, q: int) -> int:

@@ -113,6 +113,7 @@ def _signatures() -> dict:
         "fastid_abi_version": ([], i32),
         "fastid_last_error": ([], ctypes.c_char_p),
         "fastid_row_stride": ([i64], i64),
+        "fastid_launch_count": ([], ctypes.c_ulonglong),
         "fastid_max_k": ([], i32),
         "fastid_supports": ([i32, i64], i32),
         "fastid_load_words": ([vp, i64, i64, vp, i64, vp], i32),

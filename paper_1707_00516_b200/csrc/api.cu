@@ -33,6 +33,12 @@ void set_error(const char* fmt, ...) {
 
 const char* get_error() { return g_error.c_str(); }
 
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 int num_sms() {
     static std::atomic<int> cached{0};
     int n = cached.load(std::memory_order_relaxed);
@@ -334,6 +340,8 @@ __global__ void transpose_words_kernel(const uint8_t* __restrict__ src, int64_t 
 using namespace fastid;
 
 extern "C" int fastid_abi_version(void) { return FASTID_ABI_VERSION; }
+
+extern "C" unsigned long long fastid_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 #ifdef FASTID_EXPERIMENTS
 // Diagnostics (experiments build only): subsequent tensor launches record, in

@@ -30,11 +30,15 @@ const char* get_error();
                         __FILE__, __LINE__);                                                  \
     } while (0)
 
+// Kernels this library has enqueued in this process (fastid_launch_count).
+void note_launch();
+
 #define FASTID_LAUNCHED(name)                                                                   \
     do {                                                                                        \
         cudaError_t _e = cudaGetLastError();                                                    \
         if (_e != cudaSuccess)                                                                  \
             FASTID_FAIL(FASTID_E_CUDA, "launch of %s failed: %s", name, cudaGetErrorString(_e)); \
+        ::fastid::note_launch();                                                                \
     } while (0)
 
 constexpr int kMaxTopK = 32;

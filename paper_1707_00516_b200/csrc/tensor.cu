@@ -1339,6 +1339,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
             scfg.stream = side->s;
             FASTID_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
             FASTID_CUDA(cudaLaunchKernelEx(&scfg, skern, map, omap, amap, as, (const uint8_t*)a_global, tiles, n_slices));
+            note_launch();
             FASTID_CUDA(cudaEventRecord(side->join, side->s));
             FASTID_CUDA(cudaStreamWaitEvent(stream, side->join, 0));
         }

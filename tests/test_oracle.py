@@ -70,6 +70,37 @@ def test_topk_oracle_matches_reference_derivation(topk_cases):
         assert np.array_equal(hs, c["hit_score"])
 
 
+def test_scan_oracle_matches_reference_derivation(topk_cases):
+    """The database-scale oracle (row ranges on all threads, merged in row order)
+    reproduces the reference-derived top-k and threshold goldens."""
+    for c in topk_cases:
+        k = int(c["k"])
+        for workers in (1, 3, 8):
+            top, hits = oracle.scan(c["refs"], c["queries"], k, threshold=int(c["threshold"]), workers=workers)
+            assert np.array_equal(top[0], c["top_scores"]) and np.array_equal(top[1], c["top_index"]), c["name"]
+            assert np.array_equal(hits[0], c["hit_query"]) and np.array_equal(hits[1], c["hit_ref"])
+            assert np.array_equal(hits[2], c["hit_score"]) and hits[3] == len(c["hit_query"])
+
+
+@pytest.mark.parametrize("width", [32, 64])
+def test_scan_oracle_matches_topk_oracle(rng, width):
+    """Ties across row ranges, score caps, k larger than the panel, 32-bit words,
+    partial row blocks: the scan oracle equals the per-unknown oracle."""
+    for n_r, n_q, L in ((3, 4, 64), (700, 19, 1000), (2049, 7, 5000)):
+        nw = -(-L // width)
+        r, _ = rand_words(rng, n_r, nw, width, L)
+        q, _ = rand_words(rng, n_q, nw, width, L)
+        r[n_r // 2:] = r[: n_r - n_r // 2]  # every row duplicated across the two halves
+        q[: n_q // 2] = r[rng.integers(0, n_r, n_q // 2)]
+        for k, ms in ((1, 0xFFFFFFFF), (16, 0xFFFFFFFF), (32, L // 3), (5, 0)):
+            top, _ = oracle.scan(r, q, k, ms, workers=6)
+            for a, b in zip(top, oracle.topk(r, q, k, ms)):
+                assert np.array_equal(a, b), (n_r, n_q, L, k, ms)
+        _, hits = oracle.scan(r, q, 0, threshold=L // 4, workers=5)
+        exp = oracle.threshold(r, q, L // 4)
+        assert hits[3] == exp[3] and all(np.array_equal(a, b) for a, b in zip(hits[:3], exp[:3]))
+
+
 def test_topk_max_score_and_small_panels(rng):
     r, L = rand_words(rng, 50, 2, 64)
     q, _ = rand_words(rng, 9, 2, 64)
