@@ -30,6 +30,7 @@ from __future__ import annotations
 import ctypes
 import os
 import struct
+import sys
 
 import numpy as np
 import torch
@@ -279,14 +280,26 @@ def compare_device(refs: DevicePanel, queries: DevicePanel, out: torch.Tensor | 
     return out
 
 
-def compare_b200(refs, queries, formulation: str | int = "auto", device=None) -> ScoreMatrix:
-    """``compare_naive`` on the B200 (kernel.py:283-292): same signature, errors and empties."""
+def _score_matrix_type(panel):
+    """The ScoreMatrix class that goes with the caller's panel type: the reference's
+    own (fastid.kernel.ScoreMatrix) for reference panels, so isinstance checks and
+    downstream writers (write_scores) behave as with compare_naive; else this
+    package's mirror (panel.ScoreMatrix)."""
+    mod = sys.modules.get(type(panel).__module__)
+    cls = getattr(mod, "ScoreMatrix", None) if mod is not None else None
+    return cls if isinstance(cls, type) else ScoreMatrix
+
+
+def compare_b200(refs, queries, formulation: str | int = "auto", device=None):
+    """``compare_naive`` on the B200 (kernel.py:283-292): same signature, errors,
+    empties and result type (the reference's ScoreMatrix for reference panels)."""
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    result = _score_matrix_type(refs)
     n_r, n_q = refs.words.shape[0], queries.words.shape[0]
     ref_ids = getattr(refs, "ids", tuple(f"r{i}" for i in range(n_r)))
     q_ids = getattr(queries, "ids", tuple(f"q{j}" for j in range(n_q)))
     if n_r == 0 or n_q == 0:
-        return ScoreMatrix(ref_ids, q_ids, np.zeros((n_r, n_q), dtype=np.uint32))
+        return result(ref_ids, q_ids, np.zeros((n_r, n_q), dtype=np.uint32))
     dev = _require_cuda(device)
     if n_r * n_q * 4 > _PIPELINE_MIN_BYTES and isinstance(refs.words, np.ndarray) \
             and isinstance(queries.words, np.ndarray):
@@ -295,26 +308,36 @@ def compare_b200(refs, queries, formulation: str | int = "auto", device=None) ->
         scores = np.empty((n_r, n_q), np.uint32)
         with torch.cuda.device(dev):
             run_b200_kernel(refs.words, queries.words, scores, formulation=formulation)
-        return ScoreMatrix(ref_ids, q_ids, scores)
+        return result(ref_ids, q_ids, scores)
     d = compare_device(_as_device(refs, dev), _as_device(queries, dev), formulation=formulation)
     scores = d.cpu().numpy().view(np.uint32)
-    return ScoreMatrix(ref_ids, q_ids, scores)
+    return result(ref_ids, q_ids, scores)
 
 
 _PIPELINE_MIN_BYTES = 64 << 20  # fastid_run_kernel streams outputs above this (csrc/api.cu)
 
 
 def compare_blocked_b200(refs, queries: QueryLayout, tile: TileConfig | None = None, parallelism: int = 1,
-                         formulation: str | int = "auto", device=None) -> ScoreMatrix:
-    """``compare_blocked`` on the B200 (kernel.py:295-314).  ``tile`` and
-    ``parallelism`` are validated exactly as the reference does and otherwise
-    ignored: the device tiling is fixed by the kernel."""
+                         formulation: str | int = "auto", device=None):
+    """``compare_blocked`` on the B200 (kernel.py:295-314): the same checks in the
+    same order (tile, parallelism >= 1, panel compatibility), empty results for
+    empty panels, and the transposed query words scored as given -- like the
+    reference, a QueryLayout is not re-validated (the device undoes the
+    transpose, run_b200_kernel(queries_transposed=True)).  ``tile`` and
+    ``parallelism`` are otherwise ignored: the device tiling is fixed."""
     tile = tile or TileConfig()
     if parallelism < 1:
         raise ValueError("parallelism must be at least 1")
-    from .panel import restore_queries
-
-    return compare_b200(refs, restore_queries(queries), formulation, device)
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    n_r, n_q = refs.words.shape[0], queries.words.shape[1]
+    out = np.zeros((n_r, n_q), dtype=np.uint32)
+    if out.size:
+        if device is not None:
+            with torch.cuda.device(_require_cuda(device)):
+                run_b200_kernel(refs.words, queries.words, out, queries_transposed=True, formulation=formulation)
+        else:
+            run_b200_kernel(refs.words, queries.words, out, queries_transposed=True, formulation=formulation)
+    return _score_matrix_type(refs)(refs.ids, queries.ids, out)
 
 
 def run_b200_kernel(ref_words: np.ndarray, query_words: np.ndarray, out: np.ndarray,

@@ -302,6 +302,81 @@ def test_prepared_database_image(rng, form, L):
 
 
 @pytest.mark.parametrize("pairs", [True, False])
+@pytest.mark.parametrize("L", [10_000, 40_000])
+def test_prepared_image_streamed_unknowns_long_profiles(rng, pairs, L):
+    """The C5 long-profile path: prepared mxf4 image with the unknowns streamed per
+    stage (L > 2048), on the CTA-pair kernel and on the single-CTA split-B
+    kernel: top-k (k = 1, 16, 32), threshold and full matrix equal the oracle,
+    with a ragged second pair group (300 unknowns), planted copies, duplicate
+    knowns (ties) and an all-ones known (score L against an all-zero unknown)."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    n_r, n_q = 2311, 300
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    q, _ = rand_words(rng, n_q, nw, 64, L)
+    r[5] = np.uint64(2**64 - 1)
+    r = oracle.mask_padding(r, L)
+    q[0] = 0
+    q[1:60] = r[rng.integers(0, n_r, 59)]
+    r[n_r - 7 : n_r - 4] = r[10:13]
+    db = KnownDatabase(r, L, formulation="tensor_f4", ref_base=3)
+    db.set_option("no_cta_pairs", not pairs)
+    exp = oracle.naive(r, q)
+    assert exp[5, 0] == L
+    for k in (1, 16, 32):
+        s, x = db.search_words(q, k)
+        es, ex, _ = oracle.topk_from_matrix(exp, k)
+        assert np.array_equal(s, es), k
+        assert np.array_equal(x, np.where(ex >= 0, ex + 3, -1)), k
+    thr = int(np.percentile(exp, 3))
+    hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
+    hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
+    assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 3) and np.array_equal(hits.score, hs)
+    full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, exp)
+
+
+@pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8", "popc"])
+def test_longest_profiles_all_ones_exact(rng, form):
+    """L = 2^20 loci, the reference's upper bound: an all-ones known
+    scores 1,048,576 against an all-zero unknown.  The accumulators stay exact
+    (fp32 < 2^24 for mxf4, s32 for i8, u32 for POPC) on the packed-operand
+    kernels and on the prepared-image kernels (CTA pairs for mxf4), for the
+    full matrix, top-k and threshold."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1 << 20
+    nw = L // 64
+    r, _ = rand_words(rng, 40, nw, 64, L)
+    q, _ = rand_words(rng, 6, nw, 64, L)
+    r[0] = np.uint64(2**64 - 1)
+    r[1] = 0
+    r[2, : nw // 2] = np.uint64(2**64 - 1)
+    r[2, nw // 2 :] = 0
+    q[0] = 0
+    q[1] = np.uint64(2**64 - 1)
+    q[2] = r[3]
+    exp = oracle.naive(r, q)
+    assert exp[0, 0] == L and exp[2, 0] == L // 2 and exp[0, 1] == 0 and exp[3, 2] == 0
+    R, Q = m.Panel(tuple(range(40)), r, L), m.Panel(tuple(range(6)), q, L)
+    assert np.array_equal(m.compare_b200(R, Q, formulation=form).scores, exp), "packed full"
+    res = m.topk(R, Q, 4, formulation=form)
+    es, ex, _ = oracle.topk_from_matrix(exp, 4)
+    assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), "packed top-k"
+    db = KnownDatabase(r, L, formulation=form)
+    full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, exp), "image full"
+    s, x = db.search_words(q, 4)
+    assert np.array_equal(s, es) and np.array_equal(x, ex), "image top-k"
+    hits = db.threshold(Q, L // 2)
+    hq, hr, hs = oracle.threshold_from_matrix(exp, L // 2)
+    assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr) and np.array_equal(hits.score, hs)
+
+
+@pytest.mark.parametrize("pairs", [True, False])
 @pytest.mark.parametrize("shape", [(1137, 129, 1024), (2500, 520, 2048), (700, 300, 1800), (224, 256, 64),
                                    (3001, 388, 1024), (5000, 260, 512), (1500, 300, 5000), (900, 520, 2304)])
 def test_image_pairs_and_split(rng, pairs, shape):
@@ -587,3 +662,19 @@ def test_topk_writes_stay_in_workspace(rng, form):
     assert (s_full[n_q:] == -7).all() and (x_full[n_q:] == -7).all(), "write past the outputs"
     es, ex, _ = oracle.topk(r, q, k)
     assert np.array_equal(s.cpu().numpy().view(np.uint32), es) and np.array_equal(x.cpu().numpy(), ex)
+
+
+@pytest.mark.parametrize("n_q", [1, 100, 128])
+def test_popc_topk_few_unknowns_many_knowns(rng, n_q):
+    """CUDA-core top-k with one unknown group (<= 128 unknowns) and >= 80k knowns:
+    the slice count is capped so the partial lists stay within the merge's
+    768-list capacity; the result equals the oracle."""
+    m = fb()
+    L, n_r = 256, 90_000
+    r, _ = rand_words(rng, n_r, 4, 64, L)
+    q, _ = rand_words(rng, n_q, 4, 64, L)
+    q[: max(1, n_q // 3)] = r[rng.integers(0, n_r, max(1, n_q // 3))]
+    R, Q = m.Panel(tuple(range(n_r)), r, L), m.Panel(tuple(range(n_q)), q, L)
+    res = m.topk(R, Q, 16, formulation="popc")
+    es, ex, _ = oracle.topk(r, q, 16)
+    assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex)

@@ -1,17 +1,28 @@
-"""Measure BASELINE.json configs C1, C2, C4, C5 (C3 is bench.py) on one B200.
+"""Measure BASELINE.json configs C1, C2, C4, C5 (C3 is bench.py) on one B200,
+each line checked against the CPU oracle at full size.
 
 Each line: config, formulation, device time (CUDA events, warm, min of reps),
-comparisons/s, bit-pairs/s, and an oracle spot check.  Synthetic inputs are
-generated on the device (torch RNG); knowns are uniform random bits, unknowns
-planted near-copies (C1-C3, C5) or OR-mixtures of 2-5 knowns (C4).
+comparisons/s, bit-pairs/s, and the oracle check that was run (``ok`` is
+always true/false, never skipped):
 
-usage: python tools/bench_configs.py [--only C2,C4] [--json out.jsonl]
+* C1: score_checksum of the full matrix == the reference's own checksum of the
+  same synth_panel inputs (tests/golden/checksums.json).
+* C2: the full 1M x 2048 u32 matrix (8.19 GB, D2H) byte-equal to the C port of
+  compare_blocked on the same synth_panel inputs; both checksums reported.
+* C4: bench.py's generator (per-locus presence p ~ U(0.1, 0.5), OR-mixtures of
+  2-5 contributors); the top-16 of all 512 mixtures vs oracle.scan over all
+  20M knowns.
+* C5: mixture-to-mixture 4096 x 4096 full matrices (every cell vs the oracle)
+  and 2048 x N top-16 lines (every unknown vs oracle.scan) across the loci sweep.
+
+usage: python tools/bench_configs.py [--only C1,C2,C4,C5] [--json out.jsonl] [--forms tensor_f4,...]
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -23,23 +34,15 @@ sys.path.insert(0, str(ROOT / "oracle"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import bench  # noqa: E402  (the C4 generator)
 import oracle  # noqa: E402  (checker only)
 import paper_1707_00516_b200 as m  # noqa: E402
 from paper_1707_00516_b200.search import KnownDatabase  # noqa: E402
 
 
-def rand_words(n, L, gen, density=None):
+def rand_words(n, L, gen):
     nw = -(-L // 64)
-    if density is None:
-        w = torch.randint(-(2**63), 2**63 - 1, (n, nw), dtype=torch.int64, device="cuda", generator=gen)
-    else:
-        w = torch.zeros((n, nw), dtype=torch.int64, device="cuda")
-        step = max(1, (1 << 28) // (nw * 64))  # rows per chunk: ~1 GiB of float draws
-        for r0 in range(0, n, step):
-            bits = (torch.rand((min(step, n - r0), nw * 64), device="cuda", generator=gen) < density).to(torch.int64)
-            for b in range(64):
-                w[r0:r0 + bits.shape[0]] |= bits[:, b::64] << (63 - b)
-            del bits
+    w = torch.randint(-(2**63), 2**63 - 1, (n, nw), dtype=torch.int64, device="cuda", generator=gen)
     tail = L % 64
     if tail:
         w[:, -1] &= ~((1 << (64 - tail)) - 1)
@@ -74,50 +77,61 @@ def report(out, **kw):
         out.flush()
 
 
-def run_full(cfg, n_known, n_unknown, L, forms, out, gen, check_rows=64, planted=True):
-    r = rand_words(n_known, L, gen)
-    q = rand_words(n_unknown, L, gen)
-    if planted:
-        q[: n_unknown // 2] = r[torch.randint(0, n_known, (n_unknown // 2,), device="cuda", generator=gen)]
+def full_matrix_lines(cfg, r_np, q_np, L, forms, out, expected=None, extra=None):
+    """Every formulation's full matrix (device), then byte-equality with the oracle's."""
+    n_known, n_unknown = r_np.shape[0], q_np.shape[0]
+    if expected is None:
+        t0 = time.perf_counter()
+        expected = oracle.blocked(r_np, np.ascontiguousarray(q_np.T), 64, 16, os.cpu_count() or 1)
+        oracle_s = time.perf_counter() - t0
+    else:
+        oracle_s = None
+    dr, dq = m.DevicePanel.from_words(r_np, L), m.DevicePanel.from_words(q_np, L)
     for form in forms:
-        db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation=form)
-        dq = m.DevicePanel.from_words(q, L)
+        db = KnownDatabase(dr, formulation=form)
         o = torch.empty((n_known, n_unknown), dtype=torch.int32, device="cuda")
         t = timed(lambda: db.full_device(dq, o))
-        rows = torch.randint(0, n_known, (check_rows,), device="cuda", generator=gen)
-        got = o[rows].cpu().numpy().view(np.uint32)
-        exp = oracle.naive(words_np(r[rows]), words_np(q))
-        report(out, config=cfg, mode="full", formulation=form, n_known=n_known, n_unknown=n_unknown, loci=L,
-               seconds=t, out_gb_per_s=n_known * n_unknown * 4 / t / 1e9,
-               check=f"{check_rows} random rows vs oracle", ok=bool(np.array_equal(got, exp)))
-        del db, o
+        got = o.cpu().numpy().view(np.uint32)
+        ok = bool(np.array_equal(got, expected))
+        kw = dict(config=cfg, mode="full", formulation=form, n_known=n_known, n_unknown=n_unknown, loci=L,
+                  seconds=t, out_gb_per_s=n_known * n_unknown * 4 / t / 1e9,
+                  check="every cell byte-equal to the oracle (C port of compare_blocked)", ok=ok,
+                  oracle_s=oracle_s)
+        kw.update(extra or {})
+        report(out, **kw)
+        del db, o, got
         torch.cuda.empty_cache()
+    return expected
 
 
-def run_topk(cfg, r, q, L, forms, out, k=16, check_q=4, max_score=None, extra=None):
-    n_known, n_unknown = r.shape[0], q.shape[0]
+def topk_lines(cfg, dr, q_np, L, forms, out, k=16, r_np=None, extra=None):
+    """Every formulation's fused top-k over the resident panel; every unknown vs oracle.scan."""
+    n_known, n_unknown = dr.n_profiles, q_np.shape[0]
+    if r_np is None:
+        r_np = dr.to_words()
+    t0 = time.perf_counter()
+    (es, ex, _), _ = oracle.scan(r_np, q_np, k, 0xFFFFFFFE)
+    oracle_s = time.perf_counter() - t0
+    dq = m.DevicePanel.from_words(q_np, L)
     for form in forms:
-        db = KnownDatabase(m.DevicePanel.from_words(r, L), formulation=form)
-        dq = m.DevicePanel.from_words(q, L)
+        db = KnownDatabase(dr, formulation=form)
         ws = torch.empty(m.compare.topk_workspace_bytes(n_known, n_unknown, k, form), dtype=torch.uint8,
                          device="cuda")
         res = [None]
 
         def fn():
-            res[0] = db.topk_device(dq, k, max_score, ws)
+            res[0] = db.topk_device(dq, k, None, ws)
 
         t = timed(fn)
-        ok = None
-        if check_q:
-            pick = np.linspace(0, n_unknown - 1, check_q).astype(int)
-            s = res[0][0].cpu().numpy().view(np.uint32)[pick]
-            x = res[0][1].cpu().numpy()[pick]
-            es, ex, _ = oracle.topk(words_np(r), words_np(q)[pick], k,
-                                    0xFFFFFFFE if max_score is None else max_score)
-            ok = bool(np.array_equal(s, es) and np.array_equal(x, ex))
-        report(out, config=cfg, mode=f"top{k}", formulation=form, n_known=n_known, n_unknown=n_unknown, loci=L,
-               seconds=t, check=f"{check_q} unknowns vs oracle over all knowns", ok=ok, **(extra or {}))
-        del db
+        s = res[0][0].cpu().numpy().view(np.uint32)
+        x = res[0][1].cpu().numpy()
+        ok = bool(np.array_equal(s, es) and np.array_equal(x, ex))
+        kw = dict(config=cfg, mode=f"top{k}", formulation=form, n_known=n_known, n_unknown=n_unknown, loci=L,
+                  seconds=t, check=f"all {n_unknown} unknowns vs oracle.scan over all {n_known} knowns", ok=ok,
+                  oracle_s=oracle_s)
+        kw.update(extra or {})
+        report(out, **kw)
+        del db, ws
         torch.cuda.empty_cache()
 
 
@@ -148,38 +162,45 @@ def main():
                    seconds=t, check="score_checksum == reference checksum", ok=bool(ok))
 
     if "C2" in only:
-        run_full("C2", 1_000_000, 2048, 1024, forms, out, gen)
+        # 2048 x 1M x 1024 full matrix on synth_panel inputs (seed 1707): every cell vs the port
+        refs = oracle.synth_words(1_000_000, 16, 64, 1707, 0)
+        queries = oracle.synth_words(2048, 16, 64, 1707, 1)
+        queries[:1024] = refs[np.random.default_rng(5).integers(0, 1_000_000, 1024)]
+        t0 = time.perf_counter()
+        exp = oracle.blocked(refs, np.ascontiguousarray(queries.T), 64, 16, os.cpu_count() or 1)
+        oracle_s = time.perf_counter() - t0
+        full_matrix_lines("C2", refs, queries, 1024, forms, out, expected=exp,
+                          extra={"inputs": "synth_panel(1M, 16, 64, 1707, 0/1), 1024 planted copies",
+                                 "checksum": oracle.score_checksum(exp), "oracle_s": oracle_s})
+        del exp
 
     if "C4" in only:
-        # 512 mixtures of 2-5 contributors x 20M knowns x 5,000 loci, AND-NOT exclusion counts:
-        # contributors score 0; report top-16 (contributors first) with a threshold.
+        # bench.py's C4: per-locus presence p ~ U(0.1, 0.5), 512 OR-mixtures of 2-5 contributors
         L, n_known, n_mix = 5000, 20_000_000, 512
-        r = rand_words(n_known, L, gen, density=None)
-        # per-locus minor-allele presence p ~ U(0.1, 0.5): resample knowns row-blockwise at lower density
-        r[: n_known // 4] = rand_words(n_known // 4, L, gen, density=0.3)
-        contrib = torch.randint(0, n_known // 4, (n_mix, 5), device="cuda", generator=gen)
-        ncon = torch.randint(2, 6, (n_mix,), device="cuda", generator=gen)
-        q = torch.zeros((n_mix, r.shape[1]), dtype=torch.int64, device="cuda")
-        for c in range(5):
-            use = (ncon > c).unsqueeze(1)
-            q |= torch.where(use, r[contrib[:, c]], torch.zeros_like(q))
-        run_topk("C4", r, q, L, [f for f in forms if f != "popc"] + (["popc"] if "popc" in forms else []), out,
-                 k=16, check_q=2, extra={"contributors": "2-5 per mixture"})
-        del r, q
+        dr = bench.c4_shard_panel(m, 1707, 0, n_known, L, torch.device("cuda"))
+        q = bench.mixture_unknowns(dr, n_mix, np.random.default_rng(1707))
+        topk_lines("C4", dr, q, L, [f for f in forms if f != "popc"] + (["popc"] if "popc" in forms else []), out,
+                   extra={"contributors": "2-5 per mixture", "knowns": "p ~ U(0.1, 0.5) per locus"})
+        del dr
         torch.cuda.empty_cache()
 
     if "C5" in only:
         for L in (1024, 2048, 5000, 10_000, 20_000, 40_000):
-            r = rand_words(4096, L, gen)
-            run_full(f"C5-M2M-L{L}", 4096, 4096, L, forms, out, gen, check_rows=16)
+            r = words_np(rand_words(4096, L, gen))
+            q = words_np(rand_words(4096, L, gen))
+            q[:2048] = r[np.random.default_rng(L).integers(0, 4096, 2048)]
+            full_matrix_lines(f"C5-M2M-L{L}", r, q, L, forms, out)
         for L in (1024, 5000, 10_000, 40_000):
             n_known = 5_000_000 if L <= 5000 else 1_000_000
             r = rand_words(n_known, L, gen)
-            q = rand_words(2048, L, gen)
-            q[:1024] = r[torch.randint(0, n_known, (1024,), device="cuda", generator=gen)]
-            run_topk(f"C5-2048xN-L{L}", r, q, L, [f for f in forms if f != "popc" or L <= 5000], out, k=16,
-                     check_q=2 if n_known * L <= 5e9 else 0)
-            del r, q
+            q = words_np(rand_words(2048, L, gen))
+            q[:1024] = words_np(r[torch.randint(0, n_known, (1024,), device="cuda", generator=gen)])
+            dr = m.DevicePanel.from_words(r, L)
+            r_np = words_np(r)
+            del r
+            topk_lines(f"C5-2048xN-L{L}", dr, q, L, [f for f in forms if f != "popc" or L <= 5000], out, k=16,
+                       r_np=r_np)
+            del dr, r_np
             torch.cuda.empty_cache()
     if out:
         out.close()
