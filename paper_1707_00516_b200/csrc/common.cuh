@@ -146,6 +146,8 @@ struct CompareArgs {
     // CTA-pair kernel: per (slice, unknown group) tile progress, for drift control
     int* progress;
     int n_groups;
+    int drift_tiles;  // max lead (tiles) of a pair over the slowest pair of its slice
+    int drift_every;  // tiles between progress checks
     int tma_out;  // full matrix through TMA tensor stores: 1 per-warp blocks, 2 per-split blocks (set by the launcher)
     // CTA-pair kernel: spare pairs and the tiles the regular slices cover (the rest go to spares)
     int n_spare;

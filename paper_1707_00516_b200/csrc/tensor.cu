@@ -47,7 +47,8 @@ constexpr int kStageBytesPacked = 32;  // packed bytes per known row per stage (
 constexpr int kWordsPerStage = kStageBytesPacked / 4;
 constexpr int kMaxPackedStages = 12;
 constexpr int kMinPackedStages = 4;
-constexpr int kMaxUnpackedStages = 8;
+constexpr int kMaxUnpackedStages = 12;  // barrier slots; dual-tile pairs use up to 12 ring stages
+constexpr int kDefaultUnpackedStages = 8;
 constexpr int kMaxAStages = 8;
 // Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
 // highest warp ids (the scheduler favours higher ids), converters the lowest.
@@ -71,7 +72,14 @@ struct Roles {
 // insertions) does not stall the tensor pipe.
 constexpr int kAccBufs = 2;
 
-constexpr int kDriftTiles = 40;  // max lead of a pair over the slowest pair of its slice
+// Drift control: the pairs of one slice may lead the slowest of them by at
+// most drift_tiles tiles, so a tile half fetched from HBM by the first of them
+// is still in L2 when the last one reads it.  The window is sized in bytes:
+// all slices' windows together stay well inside the 126 MB L2 (C3, 4 stages
+// per tile: 40 tiles; C4, 20 stages: 2 tiles -- with the 40-tile window
+// of round 1 the two C4 groups re-read 1.75x the 51 GB image from HBM).
+constexpr int kDriftTilesMax = 40;
+constexpr int64_t kDriftWindowBytes = 48ll << 20;
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
 constexpr int kMaxSplits = 4;      // epilogue warps per TMEM lane quadrant
 constexpr int kSmemLimit = 227 * 1024;
@@ -256,6 +264,7 @@ struct Layout {
     int off_u, off_p, off_bar, total;
     int out_bytes;  // full-matrix TMA-store staging (image kernels): one [cols][32] u32 block per epilogue warp
     int off_out;
+    int su_max;  // operand-ring depth cap
     __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false, bool pair = false,
                                int stage_out = 0) {
         n_kst = (int)((stride + kStageBytesPacked - 1) / kStageBytesPacked);
@@ -263,6 +272,21 @@ struct Layout {
         out_bytes = stage_out;
         ub = pair ? kUnpackedStageBytes / 2 : kUnpackedStageBytes;
         sa = 0;
+        su_max = kDefaultUnpackedStages;
+        if (stream_a && image && pair) {
+            // dual-tile pairs consume two operand stages per A stage: the deepest
+            // A ring whose operand ring holds two stages per A stage
+            su_max = kMaxUnpackedStages;
+            for (sa = kMaxAStages; sa >= 2; --sa) {
+                a_bytes = sa * kAStageBytes;
+                place();
+                if (fits() && su >= 2 * sa) return;
+            }
+            sa = 2;
+            a_bytes = sa * kAStageBytes;
+            place();
+            return;
+        }
         if (!stream_a) {
             a_bytes = n_kst * kAStageBytes;
             place();
@@ -291,12 +315,12 @@ struct Layout {
         if (img) {
             // the tensor image is already in the UMMA layout: only the operand ring
             su = room / ub;
-            if (su > kMaxUnpackedStages) su = kMaxUnpackedStages;
+            if (su > su_max) su = su_max;
             sp = 0;
         } else {
             // deepest unpacked ring that still leaves kMinPackedStages TMA stages
             su = (room - kMinPackedStages * kPackedStageBytes) / kUnpackedStageBytes;
-            if (su > kMaxUnpackedStages) su = kMaxUnpackedStages;
+            if (su > su_max) su = su_max;
             sp = su >= 2 ? (room - su * kUnpackedStageBytes) / kPackedStageBytes : 0;
             if (sp > kMaxPackedStages) sp = kMaxPackedStages;
         }
@@ -338,6 +362,11 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     constexpr int HB = UB / 2;                 // one half of an image stage
     constexpr int RB = PAIR ? HB : UB;         // bytes this CTA receives per stage
     constexpr int PB = Layout<F>::kPackedStageBytes;
+    // Dual-tile CTA pairs (streamed A, long profiles): each A stage feeds the
+    // MMAs of two known tiles (one per accumulator), halving the A operand's
+    // L2->SM bytes per MAC.  The epilogue sees the same tile sequence.
+    constexpr bool kDual = PAIR && SA;
+    constexpr int kTileStep = kDual ? 2 : 1;
     using R = Roles<F, IMG>;
     constexpr int kConvThreads = 32 * R::kConvWarps;
     constexpr int kEpiWarps = R::kEpiWarps, kEpiThreads = 32 * R::kEpiWarps;
@@ -453,11 +482,15 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             for (int sg = 0; sg < n_seg; ++sg) {
             // first 128-B row of this segment's streamed-A stages (warp-uniform, hoisted)
             const int64_t a_row0 = ((int64_t)seg_group(sg) * 2 + rank) * n_kst * (AB / 128);
-            for (int64_t t = t_begin; t < t_end; ++t, ++local_t) {
-                if (prog && (local_t & 7) == 0) {
+            int next_check = 0;
+            for (int64_t t = t_begin; t < t_end; t += kTileStep) {
+                // dual-tile pairs (streamed A): tiles t and t + 1 share every A stage
+                const bool two = kDual && t + 1 < t_end;
+                if (prog && local_t >= next_check) {
+                    next_check = local_t + a.drift_every;
                     int lo = __reduce_min_sync(0xFFFFFFFFu, peer);
                     int spin = 0;
-                    for (; spin < 4096 && local_t - lo > kDriftTiles; ++spin) {
+                    for (; spin < 4096 && local_t - lo > a.drift_tiles; ++spin) {
                         __nanosleep(256);
                         lo = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
                         lo = __reduce_min_sync(0xFFFFFFFFu, lo);
@@ -504,6 +537,16 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         }
                         __syncwarp();
                         ru.next();
+                        if (two) {  // the second tile's half of the same stage
+                            producer_wait(a, &u_empty[ru.idx], ru.phase ^ 1);
+                            if (ptx::elect_one()) {
+                                if (leader) ptx::mbar_expect_tx(&u_full[ru.idx], 2 * HB);
+                                ptx::tma_load_2d_pair(sU + ru.idx * HB, &tmap, ptx::mapa(&u_full[ru.idx], 0), 0,
+                                                      (int)((((t + 1) * n_kst + ks) * 2 + rank) * (BN / 2)));
+                            }
+                            __syncwarp();
+                            ru.next();
+                        }
                         continue;
                     }
                     if (IMG) {
@@ -526,6 +569,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     }
                     __syncwarp();
                 }
+                local_t += two ? 2 : 1;
             }
             }
             if (PAIR && leader && a.progress && !spare && lane == 0)
@@ -551,9 +595,13 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     ptx::mbar_wait(a_full, (uint32_t)sg & 1u);
             }
             ptx::tc_fence_after();
-            for (int64_t t = t_begin; t < t_end; ++t, ++local) {
+            for (int64_t t = t_begin; t < t_end; t += kTileStep) {
+                const bool two = kDual && t + 1 < t_end;
                 const int acc = local % kAccBufs;
                 const uint32_t use = (uint32_t)(local / kAccBufs) & 1u;  // parity of this buffer's use
+                // the second tile of a dual step: the other accumulator
+                const int acc2 = (local + 1) % kAccBufs;
+                const uint32_t use2 = (uint32_t)((local + 1) / kAccBufs) & 1u;
                 const bool tr = trace_buf(a) && blockIdx.x == 0 && local < a.trace_tiles && lane == 0;
                 if (tr) trace_buf(a)[local * kTrSlots + kTrMmaWait] = clock64();
                 // spinning waits: the MMA warp's wake-up latency is on the critical path
@@ -561,7 +609,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 if (tr) trace_buf(a)[local * kTrSlots + kTrMmaGo] = clock64();
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
-                for (int ks = 0; ks < n_kst; ++ks, ru.next()) {
+                const uint32_t d2 = tmem + (uint32_t)(acc2 * BN);
+                for (int ks = 0; ks < n_kst; ++ks) {
                     const int s = ru.idx;
                     const int sa = ra.idx;
                     if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
@@ -580,7 +629,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                             ptx::mma_mxf4_pair_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol,
                                                       tmem + kSfbCol, ks ? 1u : 0u);
                             ptx::tc_commit_pair(&u_empty[s], 0x3);  // both halves of stage s reusable
-                            if (SA) ptx::tc_commit_pair(&ar_empty[sa], 0x3);
+                            if (SA && !two) ptx::tc_commit_pair(&ar_empty[sa], 0x3);
                         } else {
                             if (kSplitB)
                                 ptx::mma_mxf4_split_stage4(d, BN / 2, ad, bd, (uint64_t)(HB >> 4), a_step, b_step,
@@ -595,16 +644,36 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         }
                     }
                     __syncwarp();
+                    ru.next();
+                    if (two) {
+                        // the second tile against the same A stage, into the other accumulator
+                        if (ks == 0) ptx::mbar_wait(&t_empty[acc2], use2 ^ 1);
+                        const int s2 = ru.idx;
+                        ptx::mbar_wait(&u_full[s2], ru.phase);
+                        ptx::tc_fence_after();
+                        const uint64_t bd2 = b_desc0 + (uint64_t)(((uint32_t)s2 * RB) >> 4);
+                        if (ptx::elect_one()) {
+                            ptx::mma_mxf4_pair_stage4(d2, ad, bd2, a_step, b_step, idesc, tmem + kSfaCol,
+                                                      tmem + kSfbCol, ks ? 1u : 0u);
+                            ptx::tc_commit_pair(&u_empty[s2], 0x3);
+                            ptx::tc_commit_pair(&ar_empty[sa], 0x3);  // both tiles have read A stage sa
+                        }
+                        __syncwarp();
+                        ru.next();
+                    }
                     if (SA) ra.next();
                 }
                 if (ptx::elect_one()) {
-                    if (PAIR)
+                    if (PAIR) {
                         ptx::tc_commit_pair(&t_full[acc], 0x3);  // both CTAs' accumulators complete
-                    else
+                        if (two) ptx::tc_commit_pair(&t_full[acc2], 0x3);
+                    } else {
                         ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
+                    }
                 }
                 __syncwarp();
                 if (tr) trace_buf(a)[local * kTrSlots + kTrMmaIssued] = clock64();
+                local += two ? 2 : 1;
             }
             }
         }
@@ -1299,6 +1368,14 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         ap.n_spare = sp.n_spare;
         ap.t_main = sp.t_main;
         ap.progress = nullptr;
+        {
+            const int64_t window = kDriftWindowBytes / ((int64_t)n_slices * lay.n_kst * Layout<F>::kUnpackedStageBytes);
+            ap.drift_tiles = (int)std::min<int64_t>(kDriftTilesMax, std::max<int64_t>(2, window));
+#ifdef FASTID_EXPERIMENTS
+            if (const char* e = getenv("FASTID_DRIFT_TILES")) ap.drift_tiles = std::max(1, atoi(e));
+#endif
+            ap.drift_every = std::max(1, std::min(8, ap.drift_tiles / 4));
+        }
         if (2 * (pairs + sp.n_spare) <= num_sms()) {  // drift control only among co-resident pairs
             ap.progress = (int*)launch_scratch(1, (size_t)regular * sizeof(int), stream);
             if (!ap.progress) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the pair progress counters");
