@@ -9,6 +9,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -49,6 +50,20 @@ int num_sms() {
         cached.store(n, std::memory_order_relaxed);
     }
     return n;
+}
+
+cudaError_t ensure_dynamic_smem(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> set;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    int& cur = set[std::make_pair(dev, fn)];
+    if (bytes <= cur) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 namespace {

@@ -54,6 +54,11 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // Streaming multiprocessors of the current device (148 on a B200), cached.
 int num_sms();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `bytes` exceeds what
+// was already set for `fn` on the current device (the call costs 5-30 us of host
+// time; a small comparison's whole kernel is ~25 us).
+cudaError_t ensure_dynamic_smem(const void* fn, int bytes);
+
 // (score, index) lexicographic order: the canonical tie-break of every top-k
 // output (score ascending, then known index ascending).
 __device__ __forceinline__ bool before(uint32_t s0, uint32_t i0, uint32_t s1, uint32_t i1) {

@@ -180,7 +180,7 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     const int64_t n_q_tiles = ceil_div(a.n_queries, kRows);
     size_t smem = kStages * kStageBytes + (MODE == kTopK ? kRows * kScorePitch * 4 : 0);
     auto kern = popc_kernel<MODE, KP>;
-    FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FASTID_CUDA(ensure_dynamic_smem((const void*)kern, (int)smem));
     dim3 grid;
     if (MODE == kTopK) {
         grid = dim3((unsigned)(n_q_tiles * n_slices));

@@ -1338,7 +1338,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0);
     if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
     auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR, false>;
-    FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
+    FASTID_CUDA(ensure_dynamic_smem((const void*)kern, lay.total));
     hc.mark("set attribute");
     // pairs cover unknowns in groups of 256: prepare A for both halves of the last pair
     const int64_t groups = PAIR ? 2 * ceil_div(a.n_queries, 2 * kM) : ceil_div(a.n_queries, kM);
@@ -1360,7 +1360,10 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     }
     if (PAIR) {
         const int64_t pgroups = ceil_div(a.n_queries, 2 * kM);
-        const SparePlan sp = spare_plan(tiles, pgroups, n_slices, spares_disabled(a));
+        // The full matrix is HBM-write-bound: a spare grid on the 4 leftover SMs only
+        // contends for write bandwidth (C2: 1.64 ms with it, 1.44 ms without,
+        // tools/opt_ab.py), so spare pairs serve the top-k / threshold epilogues only.
+        const SparePlan sp = spare_plan(tiles, pgroups, n_slices, spares_disabled(a) || MODE == kFull);
         const int64_t regular = pgroups * n_slices;
         const int64_t pairs = regular;
         CompareArgs ap = a;
@@ -1376,7 +1379,9 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
 #endif
             ap.drift_every = std::max(1, std::min(8, ap.drift_tiles / 4));
         }
-        if (2 * (pairs + sp.n_spare) <= num_sms()) {  // drift control only among co-resident pairs
+        // drift control only among co-resident pairs, and only for runs long enough to
+        // drift (a small comparison skips the counters' memset launch)
+        if (2 * (pairs + sp.n_spare) <= num_sms() && tiles >= 64 * (int64_t)n_slices) {
             ap.progress = (int*)launch_scratch(1, (size_t)regular * sizeof(int), stream);
             if (!ap.progress) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate the pair progress counters");
             FASTID_CUDA(cudaMemsetAsync(ap.progress, 0, (size_t)regular * sizeof(int), stream));
@@ -1407,7 +1412,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
             // that follows on `stream` (the merge).  Its own instantiation keeps the
             // regular kernel free of the segment loops' registers.
             auto skern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR, true>;
-            FASTID_CUDA(cudaFuncSetAttribute(skern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
+            FASTID_CUDA(ensure_dynamic_smem((const void*)skern, lay.total));
             CompareArgs as = ap;
             as.progress = nullptr;
             as.trace = nullptr;
