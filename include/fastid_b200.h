@@ -204,6 +204,21 @@ FASTID_API int fastid_run_kernel_fd(const void* ref_words, int64_t n_refs, const
                                     int64_t n_queries, int64_t n_words, int word_bits, int queries_transposed,
                                     int fd, int formulation);
 
+/* Top-k over a known panel in HOST memory that need not fit on the device:
+ * the rows stream through the GPU in chunks of `chunk_rows` (0 = automatic,
+ * ~512 MB of packed rows), the upload of chunk c+1 overlapping the fused
+ * compare + top-k of chunk c, and every chunk's lists are merged into the
+ * running lists on the device.  Same result as fastid_compare_topk over the
+ * whole panel (global known indices = ref_base + row, ties to the lower index);
+ * row-major host words in, host top_scores [n_queries][k] (u32, 0xFFFFFFFF =
+ * empty) and top_index [n_queries][k] (i64, -1 = empty) out.  Page-locked
+ * `ref_words` upload without a staging copy.  Replaces the reference's batched
+ * pipeline over a panel larger than one batch (plan_batches scheduler.py:108-140,
+ * run_pipeline scheduler.py:270-419) for a top-k-reducing sink. */
+FASTID_API int fastid_run_topk(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries,
+                               int64_t n_words, int word_bits, int k, uint32_t max_score, int64_t ref_base,
+                               uint32_t* top_scores, int64_t* top_index, int64_t chunk_rows, int formulation);
+
 /* ---- measurement ------------------------------------------------------- */
 
 /* Pipe-peak probe (roofline denominator): launches an MMA-only (tensor

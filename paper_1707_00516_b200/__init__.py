@@ -21,6 +21,7 @@ from .compare import (
     threshold_hits,
     topk,
     topk_device,
+    topk_streamed,
 )
 from .errors import (
     CapacityError,
@@ -54,5 +55,5 @@ __all__ = [
     "PanelMismatchError", "PipelineAbortError", "QueryLayout", "ScoreMatrix", "ThresholdHits",
     "TileConfig", "TopKResult", "compare_b200", "compare_blocked_b200", "compare_device", "compare_to_fidm",
     "relayout_queries", "restore_queries", "row_stride", "run_b200_kernel", "threshold_hits",
-    "topk", "topk_device", "word_dtype", "words_per_profile",
+    "topk", "topk_device", "topk_streamed", "word_dtype", "words_per_profile",
 ]

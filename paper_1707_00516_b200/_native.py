@@ -129,6 +129,7 @@ def _signatures() -> dict:
         "fastid_merge_topk": ([vp, vp, i32, i64, i32, i32, vp, vp, vp], i32),
         "fastid_run_kernel": ([vp, i64, vp, i64, i64, i32, i32, vp, i32], i32),
         "fastid_run_kernel_fd": ([vp, i64, vp, i64, i64, i32, i32, i32, i32], i32),
+        "fastid_run_topk": ([vp, i64, vp, i64, i64, i32, i32, u32, i64, vp, vp, i64, i32], i32),
         "fastid_parse_panel": ([vp, i64, i32, i32, ctypes.POINTER(vp)], i32),
         "fastid_parsed_panel_shape": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
                                        ctypes.POINTER(i64)], i32),

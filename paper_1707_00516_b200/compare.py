@@ -494,6 +494,43 @@ def topk(refs, queries, k: int, max_score: int | None = None, formulation: str |
                       getattr(refs, "ids", None))
 
 
+def topk_streamed(refs, queries, k: int, max_score: int | None = None, formulation: str | int = "auto",
+                  chunk_rows: int = 0, ref_base: int = 0) -> TopKResult:
+    """``topk`` for a known panel kept in HOST memory, larger than the device if need be.
+
+    The panel's rows stream through the GPU in chunks (fastid_run_topk: pinned
+    double-buffered uploads overlapped with the fused compare + top-k of the
+    previous chunk, per-chunk lists merged on the device), so only one chunk
+    (``chunk_rows``; 0 = ~512 MB of packed rows) and its tensor image are
+    resident.  The result equals ``topk`` over the whole panel.  This is the
+    device-side form of the reference's batch planner + pipeline
+    (plan_batches scheduler.py:108-140, run_pipeline scheduler.py:270-419)
+    with a top-k-reducing sink.  Arguments are Panel-like objects (``words``,
+    ``bit_length``, ``word_width``, optional ``ids``) or the reference's Panel.
+    """
+    _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    L = _native.lib()
+    max_k = L.fastid_max_k()
+    if not 1 <= k <= max_k:
+        raise ValueError(f"k must be in [1, {max_k}]")
+    if chunk_rows < 0:
+        raise ValueError("chunk_rows must be >= 0")
+    rw = np.ascontiguousarray(refs.words)
+    qw = np.ascontiguousarray(queries.words)
+    n_r, n_q = rw.shape[0], qw.shape[0]
+    scores = np.empty((n_q, k), np.uint32)
+    index = np.empty((n_q, k), np.int64)
+    q_ids = getattr(queries, "ids", None) or tuple(f"q{j}" for j in range(n_q))
+    if n_q:
+        _require_cuda()
+        ms = EMPTY_SCORE - 1 if max_score is None else int(max_score)
+        _native.check(L.fastid_run_topk(
+            rw.ctypes.data if n_r else None, n_r, qw.ctypes.data, n_q, rw.shape[1], rw.dtype.itemsize * 8, k, ms,
+            int(ref_base), scores.ctypes.data, index.ctypes.data, int(chunk_rows),
+            _native.formulation_code(formulation)), "fastid_run_topk")
+    return TopKResult(tuple(q_ids), scores, index, getattr(refs, "ids", None))
+
+
 def threshold_hits(refs, queries, threshold: int, capacity: int | None = None,
                    formulation: str | int = "auto", device=None, ref_base: int = 0, image=None) -> ThresholdHits:
     """Every (unknown j, known i, score) with score <= threshold, ordered by (j, i)."""

@@ -217,6 +217,12 @@ struct HostContext {
     cudaEvent_t d2h_done[2] = {nullptr, nullptr};
     cudaEvent_t h2d_done[2] = {nullptr, nullptr};
     CopyPool* pool = nullptr;
+    // streamed top-k (fastid_run_topk): uploads on their own stream, overlapped
+    // with the comparison of the previous chunk on `stream`
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t raw_free[2] = {nullptr, nullptr};  // the comparison stream has consumed raw slot i
+    void* tk[4] = {nullptr, nullptr, nullptr, nullptr};  // aligned rows, tensor image, workspace, candidates
+    size_t tk_cap[4] = {0, 0, 0, 0};
 
     ~HostContext() {
         for (void* p : buf)
@@ -230,7 +236,26 @@ struct HostContext {
             if (h2d_done[i]) cudaEventDestroy(h2d_done[i]);
         }
         delete pool;
+        for (int i = 0; i < 2; ++i)
+            if (raw_free[i]) cudaEventDestroy(raw_free[i]);
+        for (void* p : tk)
+            if (p) cudaFree(p);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
+    }
+    // device buffer tk[slot] of at least `bytes` (contents not preserved)
+    int ensure_tk(int slot, size_t bytes) {
+        if (bytes <= tk_cap[slot]) return FASTID_OK;
+        cudaStreamSynchronize(stream);
+        if (tk[slot]) cudaFree(tk[slot]);
+        tk[slot] = nullptr;
+        tk_cap[slot] = 0;
+        if (cudaMalloc(&tk[slot], bytes) != cudaSuccess) {
+            cudaGetLastError();
+            FASTID_FAIL(FASTID_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
+        }
+        tk_cap[slot] = bytes;
+        return FASTID_OK;
     }
     int ensure_pipeline(size_t in_bytes, size_t raw_bytes, size_t rows_bytes, size_t out_bytes) {
         if (!pool) {
@@ -757,4 +782,131 @@ extern "C" int fastid_run_kernel_fd(const void* ref_words, int64_t n_refs, const
     if (fd < 0) FASTID_FAIL(FASTID_E_INVALID, "bad file descriptor %d", fd);
     return run_host(ref_words, n_refs, query_words, n_queries, n_words, word_bits, queries_transposed, nullptr, fd,
                     formulation);
+}
+
+namespace {
+constexpr size_t kStreamChunkBytes = (size_t)512 << 20;  // packed known rows per chunk (auto size)
+}  // namespace
+
+// Top-k over a known panel held in HOST memory, streamed through the device
+// chunk by chunk: the device-side analogue of the reference's batch planner
+// and staging lanes (plan_batches scheduler.py:108-140, run_pipeline
+// scheduler.py:270-419) for a panel larger than the device, with the sink
+// reducing every batch to per-unknown top-k lists.  Per chunk c (rows
+// [c*R, c*R + R)): host threads copy it into pinned slot c%2 (skipped when
+// the caller's rows are already page-locked), the copy stream uploads it,
+// the comparison stream aligns the rows, builds the chunk's tensor image,
+// runs the fused top-k kernel with ref_base + c*R, and merges the chunk's
+// lists into the running lists (ties keep the lower global index).  Upload
+// of chunk c+1 overlaps the comparison of chunk c.
+extern "C" int fastid_run_topk(const void* ref_words, int64_t n_refs, const void* query_words, int64_t n_queries,
+                               int64_t n_words, int word_bits, int k, uint32_t max_score, int64_t ref_base,
+                               uint32_t* top_scores, int64_t* top_index, int64_t chunk_rows, int formulation) {
+    if (word_bits != 32 && word_bits != 64) FASTID_FAIL(FASTID_E_INVALID, "word_bits must be 32 or 64");
+    if (n_words <= 0 || n_refs < 0 || n_queries < 0) FASTID_FAIL(FASTID_E_INVALID, "bad panel shape");
+    if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
+    if (chunk_rows < 0) FASTID_FAIL(FASTID_E_INVALID, "chunk_rows must be >= 0 (0 = automatic)");
+    if (n_queries == 0) return FASTID_OK;
+    if (!top_scores || !top_index || !query_words) FASTID_FAIL(FASTID_E_INVALID, "NULL buffer");
+    if (n_refs == 0) {  // every list empty, as fastid_compare_topk
+        for (int64_t i = 0; i < n_queries * k; ++i) {
+            top_scores[i] = 0xFFFFFFFFu;
+            top_index[i] = -1;
+        }
+        return FASTID_OK;
+    }
+    if (!ref_words) FASTID_FAIL(FASTID_E_INVALID, "NULL buffer");
+    HostContext* ctx = nullptr;
+    if (int rc = host_context(&ctx)) return rc;
+    const int wb = word_bits / 8;
+    const int64_t row_bytes = n_words * wb;
+    const int64_t bit_length = n_words * word_bits;  // zero padding bits add nothing to any score
+    const int64_t stride = row_stride_bytes(bit_length);
+    if (!fastid_supports(formulation, bit_length))
+        FASTID_FAIL(FASTID_E_UNSUPPORTED, "formulation %d cannot run %lld-bit profiles", formulation,
+                    (long long)bit_length);
+    const int f = resolve_formulation(formulation, bit_length);
+    int64_t rows = chunk_rows > 0 ? chunk_rows : std::max<int64_t>(1, (int64_t)(kStreamChunkBytes / (size_t)stride));
+    rows = std::min<int64_t>(rows, n_refs);
+    const int64_t n_chunks = ceil_div(n_refs, rows);
+    cudaStream_t st = ctx->stream;
+    if (!ctx->copy_stream && cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+        FASTID_FAIL(FASTID_E_CUDA, "cudaStreamCreate failed");
+    for (int i = 0; i < 2; ++i)
+        if (!ctx->raw_free[i] && cudaEventCreateWithFlags(&ctx->raw_free[i], cudaEventDisableTiming) != cudaSuccess)
+            FASTID_FAIL(FASTID_E_CUDA, "cudaEventCreate failed");
+    // rows already page-locked (cudaHostRegister / cudaMallocHost) upload straight from the caller's array
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, ref_words) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const size_t chunk_in = (size_t)rows * row_bytes;
+    const size_t lists_bytes = (size_t)n_queries * k * (sizeof(uint32_t) + sizeof(int64_t));
+    if (int rc = ctx->ensure_pipeline(pinned ? 0 : chunk_in, chunk_in, 16, 16)) return rc;
+    size_t ws_bytes = 0;
+    if (int rc = fastid_topk_workspace(rows, n_queries, k, f, &ws_bytes)) return rc;
+    const size_t img_bytes = f == FASTID_POPC ? 0 : tensor_image_bytes(rows, bit_length, f);
+    const size_t q_in = (size_t)n_queries * row_bytes;
+    if (int rc = ctx->ensure(0, q_in)) return rc;
+    if (int rc = ctx->ensure(2, (size_t)n_queries * stride)) return rc;
+    if (int rc = ctx->ensure_tk(0, (size_t)rows * stride)) return rc;
+    if (img_bytes)
+        if (int rc = ctx->ensure_tk(1, img_bytes)) return rc;
+    if (int rc = ctx->ensure_tk(2, ws_bytes)) return rc;
+    if (int rc = ctx->ensure_tk(3, 3 * lists_bytes + 64)) return rc;
+    // candidates: [running | chunk] lists (scores then indices), and the merge target
+    uint32_t* cand_s = (uint32_t*)ctx->tk[3];                       // [2][n_q][k]
+    int64_t* cand_i = (int64_t*)((uint8_t*)ctx->tk[3] + 2 * (size_t)n_queries * k * sizeof(uint32_t));
+    uint32_t* tmp_s = (uint32_t*)((uint8_t*)cand_i + 2 * (size_t)n_queries * k * sizeof(int64_t));
+    int64_t* tmp_i = (int64_t*)((uint8_t*)tmp_s + ((size_t)n_queries * k * sizeof(uint32_t) + 15) / 16 * 16);
+    const size_t nqk = (size_t)n_queries * k;
+    // unknowns: upload and align once
+    FASTID_CUDA(cudaMemcpyAsync(ctx->buf[0], query_words, q_in, cudaMemcpyHostToDevice, st));
+    if (int rc = fastid_load_words(ctx->buf[0], n_queries, row_bytes, ctx->buf[2], stride, st)) return rc;
+    for (int i = 0; i < 2; ++i) {  // no upload may wait on a slot event from an earlier call
+        FASTID_CUDA(cudaEventRecord(ctx->raw_free[i], st));
+        FASTID_CUDA(cudaEventRecord(ctx->h2d_done[i], ctx->copy_stream));
+    }
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const int slot = (int)(c & 1);
+        const int64_t r0 = c * rows, nr = std::min<int64_t>(rows, n_refs - r0);
+        const size_t nb = (size_t)nr * row_bytes;
+        const void* src = (const uint8_t*)ref_words + (size_t)r0 * row_bytes;
+        if (!pinned) {
+            // the slot's previous upload has left its pinned staging before it is rewritten
+            FASTID_CUDA(cudaEventSynchronize(ctx->h2d_done[slot]));
+            ctx->pool->copy(ctx->pin_in[slot], src, nb);
+            src = ctx->pin_in[slot];
+        }
+        FASTID_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->raw_free[slot], 0));
+        FASTID_CUDA(cudaMemcpyAsync(ctx->dev_slot[slot][0], src, nb, cudaMemcpyHostToDevice, ctx->copy_stream));
+        FASTID_CUDA(cudaEventRecord(ctx->h2d_done[slot], ctx->copy_stream));
+        FASTID_CUDA(cudaStreamWaitEvent(st, ctx->h2d_done[slot], 0));
+        if (int rc = fastid_load_words(ctx->dev_slot[slot][0], nr, row_bytes, ctx->tk[0], stride, st)) return rc;
+        FASTID_CUDA(cudaEventRecord(ctx->raw_free[slot], st));
+        if (img_bytes) {
+            CompareArgs a = make_args(ctx->tk[0], nr, ctx->tk[0], 0, stride, bit_length);
+            if (int rc = build_tensor_image(a, f, ctx->tk[1], st)) return rc;
+        }
+        int lists = 0, kp = 0;
+        size_t xo = 0, so = 0;
+        if (int rc = topk_partials_impl(ctx->tk[0], img_bytes ? ctx->tk[1] : nullptr, 0, nr, ctx->buf[2], n_queries,
+                                        stride, bit_length, k, max_score, ref_base + r0, ctx->tk[2], ws_bytes, f, st,
+                                        &lists, &kp, &xo, &so))
+            return rc;
+        const uint32_t* ps = (const uint32_t*)((uint8_t*)ctx->tk[2] + so);
+        const int64_t* px = (const int64_t*)((uint8_t*)ctx->tk[2] + xo);
+        if (c == 0) {
+            if (int rc = launch_merge(ps, px, lists, n_queries, kp, k, cand_s, cand_i, st)) return rc;
+            continue;
+        }
+        // this chunk's lists -> slot 1, then running (slot 0) + slot 1 -> running
+        if (int rc = launch_merge(ps, px, lists, n_queries, kp, k, cand_s + nqk, cand_i + nqk, st)) return rc;
+        if (int rc = launch_merge(cand_s, cand_i, 2, n_queries, k, k, tmp_s, tmp_i, st)) return rc;
+        FASTID_CUDA(cudaMemcpyAsync(cand_s, tmp_s, nqk * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        FASTID_CUDA(cudaMemcpyAsync(cand_i, tmp_i, nqk * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    FASTID_CUDA(cudaMemcpyAsync(top_scores, cand_s, nqk * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    FASTID_CUDA(cudaMemcpyAsync(top_index, cand_i, nqk * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FASTID_CUDA(cudaStreamSynchronize(st));
+    return FASTID_OK;
 }
