@@ -5,6 +5,7 @@ package; the oracle (oracle/) is only the checker.  Bar: bit-exact.
 """
 
 import json
+import os
 
 import numpy as np
 import pytest
@@ -678,3 +679,34 @@ def test_popc_topk_few_unknowns_many_knowns(rng, n_q):
     res = m.topk(R, Q, 16, formulation="popc")
     es, ex, _ = oracle.topk(r, q, 16)
     assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex)
+
+
+@pytest.mark.parametrize("n_r,n_q", [(22_222, 300), (38_477, 2048), (192 * 37 * 2 + 1, 512)])
+def test_dual_tile_pairs_streamed_unknowns(rng, n_r, n_q):
+    """Dual-tile CTA pairs (streamed unknowns, L > 2048: each A stage feeds two
+    known tiles): slices with odd and even tile counts, a one-tile remainder, the
+    spare-pair grid (2048 unknowns: 72 regular pairs + 2 spares), ragged unknown
+    groups -- top-k, threshold and the full matrix equal the oracle."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 5000
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    q, _ = rand_words(rng, n_q, nw, 64, L)
+    q[:40] = r[rng.integers(0, n_r, 40)]
+    r[-2:] = r[:2]  # ties across the first and last tiles
+    db = KnownDatabase(r, L, formulation="tensor_f4")
+    for k in (16, 5):
+        s, x = db.search_words(q, k)
+        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE)
+        assert np.array_equal(s, es), (n_r, n_q, k)
+        assert np.array_equal(x, ex), (n_r, n_q, k)
+    if n_r * n_q <= 50_000_000:
+        exp = oracle.blocked(r, np.ascontiguousarray(q.T), 64, 16, os.cpu_count() or 1)
+        thr = int(np.percentile(exp[:, :8], 1))
+        hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
+        hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
+        assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr) and np.array_equal(hits.score, hs)
+        full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+        assert np.array_equal(full, exp)
