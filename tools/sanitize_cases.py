@@ -55,6 +55,28 @@ def main():
         assert np.array_equal(hits.query, jj) and np.array_equal(hits.ref, ii), (L, "threshold hits")
         assert np.array_equal(hits.score, expected.T[jj, ii]), (L, "threshold scores")
         n_cases += 3
+    # dual-tile CTA pairs (streamed unknowns, >= 2 tiles per slice, odd remainder)
+    refs, queries = panel(rng, 192 * 74 * 2 + 193, 5000, "r"), panel(rng, 40, 5000, "q")
+    expected = oracle.naive(refs.words, queries.words)
+    db = KnownDatabase(refs)
+    s, x = db.search_words(queries.words, 16)
+    es, ex, _ = oracle.topk_from_matrix(expected, 16)
+    assert np.array_equal(s, es) and np.array_equal(x, ex), "dual-tile topk"
+    out = torch.full((refs.words.shape[0], 40), -1, dtype=torch.int32, device="cuda")
+    full = db.full_device(fb.DevicePanel.from_panel(queries), out).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, expected), "dual-tile full"
+    thr = int(np.percentile(expected, 1))
+    hits = db.threshold(queries, thr)
+    jj, ii = np.nonzero(expected.T <= thr)
+    assert np.array_equal(hits.query, jj) and np.array_equal(hits.ref, ii), "dual-tile threshold"
+    n_cases += 3
+    # out-of-core top-k: host panel streamed in chunks (copy stream + device merge)
+    refs, queries = panel(rng, 5000, 1024, "r"), panel(rng, 70, 1024, "q")
+    expected = oracle.naive(refs.words, queries.words)
+    res = fb.topk_streamed(refs, queries, 8, chunk_rows=1500)
+    es, ex, _ = oracle.topk_from_matrix(expected, 8)
+    assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), "streamed topk"
+    n_cases += 1
     torch.cuda.synchronize()
     print(f"sanitize cases ok ({n_cases})")
 
