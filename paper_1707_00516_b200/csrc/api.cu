@@ -243,10 +243,15 @@ struct HostContext {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
+    // both streams idle: nothing in flight still reads or writes a buffer about to be freed
+    void quiesce() {
+        if (copy_stream) cudaStreamSynchronize(copy_stream);
+        cudaStreamSynchronize(stream);
+    }
     // device buffer tk[slot] of at least `bytes` (contents not preserved)
     int ensure_tk(int slot, size_t bytes) {
         if (bytes <= tk_cap[slot]) return FASTID_OK;
-        cudaStreamSynchronize(stream);
+        quiesce();
         if (tk[slot]) cudaFree(tk[slot]);
         tk[slot] = nullptr;
         tk_cap[slot] = 0;
@@ -272,7 +277,7 @@ struct HostContext {
         // capacity 0, so a later call reallocates instead of using a null slot.
         auto grow_pinned = [&](void** slots, size_t& cap, size_t bytes) -> int {
             if (bytes <= cap) return FASTID_OK;
-            cudaStreamSynchronize(stream);
+            quiesce();
             for (int i = 0; i < 2; ++i) {
                 if (slots[i]) cudaFreeHost(slots[i]);
                 slots[i] = nullptr;
@@ -296,7 +301,7 @@ struct HostContext {
         const size_t want[3] = {raw_bytes, rows_bytes, out_bytes};
         for (int j = 0; j < 3; ++j) {
             if (want[j] <= dev_slot_cap[j]) continue;
-            cudaStreamSynchronize(stream);
+            quiesce();
             for (int i = 0; i < 2; ++i) {
                 if (dev_slot[i][j]) cudaFree(dev_slot[i][j]);
                 dev_slot[i][j] = nullptr;
@@ -318,6 +323,7 @@ struct HostContext {
     }
     int ensure(int slot, size_t bytes) {
         if (bytes <= cap[slot]) return FASTID_OK;
+        quiesce();
         if (buf[slot]) cudaFree(buf[slot]);
         buf[slot] = nullptr;
         cap[slot] = 0;
@@ -866,6 +872,9 @@ extern "C" int fastid_run_topk(const void* ref_words, int64_t n_refs, const void
         FASTID_CUDA(cudaEventRecord(ctx->raw_free[i], st));
         FASTID_CUDA(cudaEventRecord(ctx->h2d_done[i], ctx->copy_stream));
     }
+    // a failure part-way leaves work in flight on both streams: drain them before
+    // returning, so no later call frees or refills a buffer still being used
+    const int rc_loop = [&]() -> int {
     for (int64_t c = 0; c < n_chunks; ++c) {
         const int slot = (int)(c & 1);
         const int64_t r0 = c * rows, nr = std::min<int64_t>(rows, n_refs - r0);
@@ -904,6 +913,12 @@ extern "C" int fastid_run_topk(const void* ref_words, int64_t n_refs, const void
         if (int rc = launch_merge(cand_s, cand_i, 2, n_queries, k, k, tmp_s, tmp_i, st)) return rc;
         FASTID_CUDA(cudaMemcpyAsync(cand_s, tmp_s, nqk * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
         FASTID_CUDA(cudaMemcpyAsync(cand_i, tmp_i, nqk * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    return FASTID_OK;
+    }();
+    if (rc_loop != FASTID_OK) {
+        ctx->quiesce();
+        return rc_loop;
     }
     FASTID_CUDA(cudaMemcpyAsync(top_scores, cand_s, nqk * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     FASTID_CUDA(cudaMemcpyAsync(top_index, cand_i, nqk * sizeof(int64_t), cudaMemcpyDeviceToHost, st));

@@ -400,7 +400,8 @@ extern "C" int fastid_probe_variant(int formulation, int variant, int iters, voi
         const bool n256 = (variant & 16) != 0;
         const bool n192 = (variant & 128) != 0;
         const bool n144 = (variant & 1024) != 0;
-        auto kern = n144 ? mma_pair_probe_kernel<144>
+        const bool n96 = (variant & 8192) != 0;
+        auto kern = n96 ? mma_pair_probe_kernel<96> : n144 ? mma_pair_probe_kernel<144>
                          : (n192 ? mma_pair_probe_kernel<192>
                                  : (n256 ? mma_pair_probe_kernel<256> : mma_pair_probe_kernel<224>));
         FASTID_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -421,7 +422,7 @@ extern "C" int fastid_probe_variant(int formulation, int variant, int iters, voi
                                                              ((variant & 64) ? 8 : 0) | ((variant & 256) ? 16 : 0) | ((variant & 512) ? 32 : 0) |
                                                              ((variant & 2048) ? 64 : 0) | ((variant & 4096) ? 128 : 0)));
         FASTID_LAUNCHED("mma_pair_probe_kernel");
-        *work = (double)(sms / 2) * iters * 256.0 * (n144 ? 144 : (n192 ? 192 : (n256 ? 256 : 224))) * 64.0;
+        *work = (double)(sms / 2) * iters * 256.0 * (n96 ? 96 : (n144 ? 144 : (n192 ? 192 : (n256 ? 256 : 224)))) * 64.0;
         return FASTID_OK;
     }
     const int bn = f4 ? 224 : 128;

@@ -100,6 +100,7 @@ class QueryStager:
         self.host_s = torch.empty((n_queries, k), dtype=torch.int32).pin_memory()
         self.host_x = torch.empty((n_queries, k), dtype=torch.int64).pin_memory()
         self.workspace = None
+        self.done = torch.cuda.Event()  # recorded after this stager's D2H (pipelined searches)
 
     @property
     def h2d_bytes(self) -> int:
@@ -181,8 +182,8 @@ class KnownDatabase:
         return compare_device(self.panel, queries, out, self.formulation, image=self.image)
 
     # -- host-buffer public calls ------------------------------------------------
-    def stager(self, n_queries: int, k: int) -> QueryStager:
-        key = (n_queries, k)
+    def stager(self, n_queries: int, k: int, slot: int = 0) -> QueryStager:
+        key = (n_queries, k, slot)
         st = self._stagers.get(key)
         if st is None:
             p = self.panel
@@ -238,6 +239,41 @@ class KnownDatabase:
         with torch.cuda.device(self.device):
             s, x = self.topk_device(st.panel, k, max_score, st.workspace, (st.out_s, st.out_x))
         return self.fetch_lists(st, s, x)
+
+    def search_many(self, batches, k: int = 16, max_score: int | None = None, combine=None):
+        """Pipelined top-k over a sequence of host query batches (a serving loop):
+        batch i+1 is staged (pinned copy, H2D, encode) and its kernels enqueued
+        before batch i's lists are read back, so the host work and the D2H of one
+        batch overlap the device work of the next.  Yields host (scores, index)
+        per batch, in order; each equals ``search_words`` of that batch.
+        ``combine(s, x, k)`` is applied on the device before the read-back (the
+        sharded driver's cross-rank gather + merge)."""
+        stream = torch.cuda.current_stream(self.device)
+        pending = None
+        slot = 0
+        for qw in batches:
+            qw = np.ascontiguousarray(qw)
+            st = self.stager(qw.shape[0], k, slot)
+            st.done.synchronize()  # the slot's previous batch has been read back
+            self.stage_queries(qw, k, st)
+            with torch.cuda.device(self.device):
+                s, x = self.topk_device(st.panel, k, max_score, st.workspace, (st.out_s, st.out_x))
+                if combine is not None:
+                    s, x = combine(s, x, k)
+                st.host_s.copy_(s, non_blocking=True)
+                st.host_x.copy_(x, non_blocking=True)
+                st.done.record(stream)
+            if pending is not None:
+                yield self._read_back(pending)
+            pending = st
+            slot ^= 1
+        if pending is not None:
+            yield self._read_back(pending)
+
+    @staticmethod
+    def _read_back(st: QueryStager) -> tuple[np.ndarray, np.ndarray]:
+        st.done.synchronize()
+        return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
 
     def search(self, queries, k: int = 16, max_score: int | None = None) -> TopKResult:
         """Per unknown, the k closest knowns by (score asc, global index asc)."""

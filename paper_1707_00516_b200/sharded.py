@@ -154,6 +154,12 @@ class ShardedDatabase:
         s, x = self.local.topk_device(queries, k, max_score, workspace, out)
         return self.combine(s, x, k)
 
+    def search_many(self, batches, k: int = 16, max_score: int | None = None):
+        """Pipelined global top-k over a sequence of host query batches (every rank
+        passes the same batches): KnownDatabase.search_many with the cross-rank
+        gather + merge on the device before each read-back."""
+        return self.local.search_many(batches, k, max_score, combine=self.combine)
+
     def search_words(self, query_words: np.ndarray, k: int = 16, max_score: int | None = None):
         """Host unknowns -> global top-k (host arrays) on every rank."""
         db = self.local

@@ -710,3 +710,25 @@ def test_dual_tile_pairs_streamed_unknowns(rng, n_r, n_q):
         assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr) and np.array_equal(hits.score, hs)
         full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
         assert np.array_equal(full, exp)
+
+
+def test_search_many_pipelined(rng):
+    """KnownDatabase.search_many (batch i+1 staged before batch i is read back):
+    every batch's lists equal the oracle's, across changing contents, a changing
+    batch shape (new stagers mid-stream) and k."""
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L, n_r = 1024, 20_000
+    r, _ = rand_words(rng, n_r, 16, 64, L)
+    db = KnownDatabase(r, L)
+    batches = []
+    for n_q in (256, 256, 100, 256, 256):
+        q, _ = rand_words(rng, n_q, 16, 64, L)
+        q[:10] = r[rng.integers(0, n_r, 10)]
+        batches.append(q)
+    got = list(db.search_many(batches, 8))
+    assert len(got) == len(batches)
+    for q, (s, x) in zip(batches, got):
+        es, ex, _ = oracle.topk(r, q, 8, 0xFFFFFFFE)
+        assert np.array_equal(s, es) and np.array_equal(x, ex)
+    assert list(db.search_many([], 8)) == []

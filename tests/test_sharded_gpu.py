@@ -42,7 +42,9 @@ def _worker(rank, world, port, refs, queries, L, k, result_q):
     from paper_1707_00516_b200.panel import Panel
 
     hits = db.threshold(Panel(tuple(range(len(queries))), queries, L), L // 8)
-    result_q.put((rank, s, x, hits.query, hits.ref, hits.score))
+    # the pipelined serving loop over three batches (global lists per batch)
+    many = list(db.search_many([queries, queries[::-1].copy(), queries], k))
+    result_q.put((rank, s, x, hits.query, hits.ref, hits.score, many))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -72,8 +74,11 @@ def test_sharded_two_ranks_real_kernels(rng):
     es, ex, _ = oracle.topk(refs, queries, k)
     hq, hr, hs, _ = oracle.threshold(refs, queries, L // 8)
     assert len(hq) >= 52
-    for rank, s, x, tq, tr, ts in out:
+    for rank, s, x, tq, tr, ts, many in out:
         assert np.array_equal(s, es) and np.array_equal(x, ex), rank
+        assert len(many) == 3
+        for (ms, mx), (e_s, e_x) in zip(many, ((es, ex), (es[::-1], ex[::-1]), (es, ex))):
+            assert np.array_equal(ms, e_s) and np.array_equal(mx, e_x), rank
         # threshold hits of both shards: count exchange + padded gather, (j, i) order
         assert np.array_equal(tq, hq) and np.array_equal(tr, hr) and np.array_equal(ts, hs), rank
     assert 7 in ex[50] and n_r // 2 + 5 in ex[50]

@@ -10,12 +10,16 @@ scratch = torch.zeros(4096, dtype=torch.int32, device="cuda")
 src = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
 B = 268
 names = {}
-for nflag, n in ((128, "N=192"), (1024, "N=144")):
+for nflag, n in ((128, "N=192"), (1024, "N=144"), (8192, "N=96")):
     for extra, nm in ((0, "plain"), (64 + 512, "wait+commit/4"), (64 + 512 + 2048, "wait+commit/8"),
                       (64 + 512 + 4096, "wait+commit/4 3buf"), (64 + 512 + 2048 + 4096, "wait+commit/8 3buf")):
         if nflag == 128 and extra & 4096:
             continue
+        if nflag == 8192 and extra not in (0, 64 + 512):
+            continue
         names[B + nflag + extra] = f"pair {n} tiled {nm}"
+for nflag, n in ((128, "N=192"), (8192, "N=96"), (16, "N=256")):
+    names[8 + 4 + 32 + nflag] = f"pair {n} 2 accumulators alternating, random operands"
 for variant, name in names.items():
     best = 0
     for rep in range(4):
