@@ -153,6 +153,8 @@ struct CompareArgs {
     int n_groups;
     int drift_tiles;  // max lead (tiles) of a pair over the slowest pair of its slice
     int drift_every;  // tiles between progress checks
+    int dual_lag;     // dual-tile pairs: stages the second tile lags the first (-1 = default)
+    int dual_sa;      // dual-tile pairs: A ring depth (0 = default)
     int tma_out;  // full matrix through TMA tensor stores: 1 per-warp blocks, 2 per-split blocks (set by the launcher)
     // CTA-pair kernel: spare pairs and the tiles the regular slices cover (the rest go to spares)
     int n_spare;

@@ -49,6 +49,13 @@ constexpr int kMaxPackedStages = 12;
 constexpr int kMinPackedStages = 4;
 constexpr int kMaxUnpackedStages = 12;  // barrier slots; dual-tile pairs use up to 12 ring stages
 constexpr int kDefaultUnpackedStages = 8;
+// Dual-tile pairs: the second tile lags the first by kDualLag stages, and the
+// A ring keeps kDualPrefetch stages of prefetch beyond the lag (A stages are
+// L2 reads; fewer than 3 in flight stall the MMA).  A/B on one box
+// (tools/dual_ab.py, C4): A ring 7 / lag 3 reaches 13.2 ms at full clock vs
+// 13.4 ms without a lag; A ring 6 / lag 4 (prefetch 1) 18.7 ms.
+constexpr int kDualLag = 3;
+constexpr int kDualPrefetch = 3;
 constexpr int kMaxAStages = 8;
 // Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
 // highest warp ids (the scheduler favours higher ids), converters the lowest.
@@ -266,7 +273,7 @@ struct Layout {
     int off_out;
     int su_max;  // operand-ring depth cap
     __host__ __device__ Layout(int64_t stride, bool stream_a, bool image = false, bool pair = false,
-                               int stage_out = 0) {
+                               int stage_out = 0, int want_sa = 0) {
         n_kst = (int)((stride + kStageBytesPacked - 1) / kStageBytesPacked);
         img = image;
         out_bytes = stage_out;
@@ -274,13 +281,22 @@ struct Layout {
         sa = 0;
         su_max = kDefaultUnpackedStages;
         if (stream_a && image && pair) {
-            // dual-tile pairs consume two operand stages per A stage: the deepest
-            // A ring whose operand ring holds two stages per A stage
+            // dual-tile pairs: an A stage stays resident for the second tile's lag
+            // (kDualLag stages) plus kDualPrefetch stages of prefetch, and the operand
+            // ring holds two stages per A stage in flight: the deepest A ring up to
+            // kDualLag + 1 + kDualPrefetch whose operand ring still has sa + 2 stages
             su_max = kMaxUnpackedStages;
-            for (sa = kMaxAStages; sa >= 2; --sa) {
+            if (want_sa >= 2 && want_sa <= kMaxAStages) {
+                sa = want_sa;
                 a_bytes = sa * kAStageBytes;
                 place();
-                if (fits() && su >= 2 * sa) return;
+                if (fits()) return;
+            }
+            for (sa = kDualLag + 1 + kDualPrefetch < kMaxAStages ? kDualLag + 1 + kDualPrefetch : kMaxAStages; sa >= 3;
+                 --sa) {
+                a_bytes = sa * kAStageBytes;
+                place();
+                if (fits() && su >= sa + 2) return;
             }
             sa = 2;
             a_bytes = sa * kAStageBytes;
@@ -367,17 +383,26 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     // L2->SM bytes per MAC.  The epilogue sees the same tile sequence.
     constexpr bool kDual = PAIR && SA;
     constexpr int kTileStep = kDual ? 2 : 1;
+    // The second tile of a dual step lags the first by `lag` stages: the first
+    // tile's accumulator completes `lag` stages early and drains while the MMA
+    // pipe finishes the second (and the second's drains while the next first
+    // tile runs its first `lag` stages), so the pipe never waits for a buffer.
+    // Each A stage stays in the ring for `lag` stages (ring depth >= lag + 2).
     using R = Roles<F, IMG>;
     constexpr int kConvThreads = 32 * R::kConvWarps;
     constexpr int kEpiWarps = R::kEpiWarps, kEpiThreads = 32 * R::kEpiWarps;
     constexpr int kBuildWarps = R::kBuildWarps;
     constexpr int kFirstEpiWarp = R::kFirstEpiWarp, kProducerWarp = R::kProducerWarp, kMmaWarp = R::kMmaWarp;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0);
+    const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0, a.dual_sa);
     constexpr int AB = Layout<F>::kAStageBytes;
     const int SP = lay.sp;
     const int SU = lay.su;
     const int n_kst = lay.n_kst;
+    const int lag = !kDual ? 0
+                           : max(0, min(a.dual_lag >= 0 ? min(a.dual_lag, lay.sa - 2)
+                                                        : min(kDualLag, lay.sa - 1 - kDualPrefetch),
+                                        n_kst));
     uint8_t* sA = smem;
     uint8_t* sU = smem + lay.off_u;
     uint8_t* sP = smem + lay.off_p;
@@ -479,6 +504,18 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             // so their latency never stalls the operand stream.
             int local_t = 0;
             int peer = 0x7FFFFFFF;  // this lane's peer counter, in flight since the last check
+            // this CTA's half of known tile `tile`, stage `ks` (tensor map over the image,
+            // box = one half); completion is counted on the leader's barrier, which expects both
+            auto load_half = [&](int64_t tile, int ks, Ring& r) {
+                producer_wait(a, &u_empty[r.idx], r.phase ^ 1);
+                if (ptx::elect_one()) {
+                    if (leader) ptx::mbar_expect_tx(&u_full[r.idx], 2 * HB);
+                    ptx::tma_load_2d_pair(sU + r.idx * HB, &tmap, ptx::mapa(&u_full[r.idx], 0), 0,
+                                          (int)(((tile * n_kst + ks) * 2 + rank) * (BN / 2)));
+                }
+                __syncwarp();
+                r.next();
+            };
             for (int sg = 0; sg < n_seg; ++sg) {
             // first 128-B row of this segment's streamed-A stages (warp-uniform, hoisted)
             const int64_t a_row0 = ((int64_t)seg_group(sg) * 2 + rank) * n_kst * (AB / 128);
@@ -501,6 +538,26 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     if (spin == 4096) prog = nullptr;
                     if (prog) peer = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
                 }
+                if constexpr (kDual) {
+                    // A stage ks and the first tile's half at step ks; the second tile's
+                    // half of stage ks - d at step ks (the MMA warp's consumption order)
+                    const int d = two ? lag : 0;
+                    for (int ks = 0; ks < n_kst + d; ++ks) {
+                        if (ks < n_kst) {
+                            const int sa = ra.idx;
+                            producer_wait(a, &ar_empty[sa], ra.phase ^ 1);
+                            if (ptx::elect_one()) {
+                                if (leader) ptx::mbar_expect_tx(&ar_full[sa], 2 * AB);
+                                ptx::tma_load_2d_pair(sA + sa * AB, &amap, ptx::mapa(&ar_full[sa], 0), 0,
+                                                      (int)(a_row0 + (int64_t)ks * (AB / 128)));
+                            }
+                            __syncwarp();
+                            ra.next();
+                            load_half(t, ks, ru);
+                        }
+                        if (two && ks >= d) load_half(t + 1, ks - d, ru);
+                    }
+                } else {
                 for (int ks = 0; ks < n_kst; ++ks, rp.next()) {
                     if (SA) {
                         // this stage's slice of the pre-unpacked A operand (one bulk copy)
@@ -537,16 +594,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         }
                         __syncwarp();
                         ru.next();
-                        if (two) {  // the second tile's half of the same stage
-                            producer_wait(a, &u_empty[ru.idx], ru.phase ^ 1);
-                            if (ptx::elect_one()) {
-                                if (leader) ptx::mbar_expect_tx(&u_full[ru.idx], 2 * HB);
-                                ptx::tma_load_2d_pair(sU + ru.idx * HB, &tmap, ptx::mapa(&u_full[ru.idx], 0), 0,
-                                                      (int)((((t + 1) * n_kst + ks) * 2 + rank) * (BN / 2)));
-                            }
-                            __syncwarp();
-                            ru.next();
-                        }
                         continue;
                     }
                     if (IMG) {
@@ -569,6 +616,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     }
                     __syncwarp();
                 }
+                }  // not dual
                 local_t += two ? 2 : 1;
             }
             }
@@ -610,6 +658,47 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 const uint32_t d2 = tmem + (uint32_t)(acc2 * BN);
+                if constexpr (kDual) {
+                    constexpr uint64_t a_step = (2 * kM * 16) >> 4, b_step = (2 * kBRows * 16) >> 4;
+                    const int dl = two ? lag : 0;
+                    // A ring positions of the two tiles' current stages (the second tile's
+                    // trails the first's by dl); both start at this step's first A stage
+                    Ring ay = ra;
+                    auto mma_half = [&](uint32_t dacc, int sa, int ks, bool release_a) {
+                        const int s = ru.idx;
+                        ptx::mbar_wait(&u_full[s], ru.phase);
+                        ptx::tc_fence_after();
+                        const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)sa * AB) >> 4);
+                        const uint64_t bd = b_desc0 + (uint64_t)(((uint32_t)s * RB) >> 4);
+                        if (ptx::elect_one()) {
+                            ptx::mma_mxf4_pair_stage4(dacc, ad, bd, a_step, b_step, idesc, tmem + kSfaCol,
+                                                      tmem + kSfbCol, ks ? 1u : 0u);
+                            ptx::tc_commit_pair(&u_empty[s], 0x3);  // both halves of stage s reusable
+                            if (release_a) ptx::tc_commit_pair(&ar_empty[sa], 0x3);
+                        }
+                        __syncwarp();
+                        ru.next();
+                    };
+                    for (int ks = 0; ks < n_kst + dl; ++ks) {
+                        if (ks < n_kst) {
+                            ptx::mbar_wait(&ar_full[ra.idx], ra.phase);
+                            mma_half(d, ra.idx, ks, !two);
+                            ra.next();
+                            if (two && ks == n_kst - 1) {
+                                // the first tile is complete: it drains while the second finishes
+                                if (ptx::elect_one()) ptx::tc_commit_pair(&t_full[acc], 0x3);
+                                __syncwarp();
+                            }
+                        }
+                        if (two && ks >= dl) {
+                            if (ks == dl) ptx::mbar_wait(&t_empty[acc2], use2 ^ 1);
+                            mma_half(d2, ay.idx, ks - dl, true);  // the A stage's last reader
+                            ay.next();
+                        }
+                    }
+                    if (ptx::elect_one()) ptx::tc_commit_pair(&t_full[two ? acc2 : acc], 0x3);
+                    __syncwarp();
+                } else {
                 for (int ks = 0; ks < n_kst; ++ks) {
                     const int s = ru.idx;
                     const int sa = ra.idx;
@@ -629,7 +718,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                             ptx::mma_mxf4_pair_stage4(d, ad, bd, a_step, b_step, idesc, tmem + kSfaCol,
                                                       tmem + kSfbCol, ks ? 1u : 0u);
                             ptx::tc_commit_pair(&u_empty[s], 0x3);  // both halves of stage s reusable
-                            if (SA && !two) ptx::tc_commit_pair(&ar_empty[sa], 0x3);
                         } else {
                             if (kSplitB)
                                 ptx::mma_mxf4_split_stage4(d, BN / 2, ad, bd, (uint64_t)(HB >> 4), a_step, b_step,
@@ -645,33 +733,16 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     }
                     __syncwarp();
                     ru.next();
-                    if (two) {
-                        // the second tile against the same A stage, into the other accumulator
-                        if (ks == 0) ptx::mbar_wait(&t_empty[acc2], use2 ^ 1);
-                        const int s2 = ru.idx;
-                        ptx::mbar_wait(&u_full[s2], ru.phase);
-                        ptx::tc_fence_after();
-                        const uint64_t bd2 = b_desc0 + (uint64_t)(((uint32_t)s2 * RB) >> 4);
-                        if (ptx::elect_one()) {
-                            ptx::mma_mxf4_pair_stage4(d2, ad, bd2, a_step, b_step, idesc, tmem + kSfaCol,
-                                                      tmem + kSfbCol, ks ? 1u : 0u);
-                            ptx::tc_commit_pair(&u_empty[s2], 0x3);
-                            ptx::tc_commit_pair(&ar_empty[sa], 0x3);  // both tiles have read A stage sa
-                        }
-                        __syncwarp();
-                        ru.next();
-                    }
                     if (SA) ra.next();
                 }
                 if (ptx::elect_one()) {
-                    if (PAIR) {
+                    if (PAIR)
                         ptx::tc_commit_pair(&t_full[acc], 0x3);  // both CTAs' accumulators complete
-                        if (two) ptx::tc_commit_pair(&t_full[acc2], 0x3);
-                    } else {
+                    else
                         ptx::tc_commit(&t_full[acc]);  // accumulator complete -> epilogue
-                    }
                 }
                 __syncwarp();
+                }  // not dual
                 if (tr) trace_buf(a)[local * kTrSlots + kTrMmaIssued] = clock64();
                 local += two ? 2 : 1;
             }
@@ -1314,6 +1385,10 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     HostClock hc(experiment(a_in, 128));
     std::lock_guard<std::mutex> launch_lock(stream_mutex(stream));
     CompareArgs a = a_in;
+    // tuning knobs of the dual-tile pair kernel's ring split (scheduling only: the
+    // result is identical for every value); FASTID_DUAL_SA = A ring depth
+    a.dual_sa = 0;
+    if (const char* e = getenv("FASTID_DUAL_SA")) a.dual_sa = atoi(e);
     CUtensorMap omap;
     memset(&omap, 0, sizeof(omap));
     a.tma_out = 0;
@@ -1335,7 +1410,7 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         if (int rc = make_known_map(&map, a, Fmt<F>::BN)) return rc;
     }
     hc.mark("tensor map");
-    const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0);
+    const Layout<F> lay(a.stride, SA, IMG, PAIR, a.tma_out ? out_stage_bytes<F, MODE, IMG, PAIR>() : 0, a.dual_sa);
     if (!lay.fits()) FASTID_FAIL(FASTID_E_UNSUPPORTED, "tile needs %d bytes of shared memory", lay.total);
     auto kern = tensor_kernel<F, MODE, KP, SA, IMG, PAIR, false>;
     FASTID_CUDA(ensure_dynamic_smem((const void*)kern, lay.total));
@@ -1374,6 +1449,8 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         {
             const int64_t window = kDriftWindowBytes / ((int64_t)n_slices * lay.n_kst * Layout<F>::kUnpackedStageBytes);
             ap.drift_tiles = (int)std::min<int64_t>(kDriftTilesMax, std::max<int64_t>(2, window));
+            ap.dual_lag = -1;  // FASTID_DUAL_LAG: stages the second tile of a dual step lags
+            if (const char* e = getenv("FASTID_DUAL_LAG")) ap.dual_lag = atoi(e);
 #ifdef FASTID_EXPERIMENTS
             if (const char* e = getenv("FASTID_DRIFT_TILES")) ap.drift_tiles = std::max(1, atoi(e));
 #endif
