@@ -55,6 +55,13 @@ constexpr int kDefaultUnpackedStages = 8;
 // (tools/dual_ab.py, C4): A ring 7 / lag 3 reaches 13.2 ms at full clock vs
 // 13.4 ms without a lag; A ring 6 / lag 4 (prefetch 1) 18.7 ms.
 constexpr int kDualLag = 3;
+constexpr int kPrefetchStages = 16;
+// The image is read by 2-D TMA boxes over a view of 2 KB rows (u64 elements, the
+// widest inner box): a half stage (12 KB) is 6 rows.  With 128-B rows (96 per
+// half) the pair kernel streamed an image that misses in L2 at 1.8 TB/s (one
+// unknown group: 5.6 ms for 20M x 1024 loci); the single-CTA kernel's 1-D bulk
+// copies reach 6.1 TB/s on the same stream.
+constexpr int kImgRowBytes = 2048;  // L2 prefetch distance of the pair kernels' known-tile stream
 constexpr int kDualPrefetch = 3;
 constexpr int kMaxAStages = 8;
 // Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
@@ -79,12 +86,15 @@ struct Roles {
 // insertions) does not stall the tensor pipe.
 constexpr int kAccBufs = 2;
 
-// Drift control: the pairs of one slice may lead the slowest of them by at
-// most drift_tiles tiles, so a tile half fetched from HBM by the first of them
-// is still in L2 when the last one reads it.  The window is sized in bytes:
-// all slices' windows together stay well inside the 126 MB L2 (C3, 4 stages
-// per tile: 40 tiles; C4, 20 stages: 2 tiles -- with the 40-tile window
-// of round 1 the two C4 groups re-read 1.75x the 51 GB image from HBM).
+// Drift control: the pairs of one slice may lead the slowest of their peers
+// by at most drift_tiles tiles, so a tile half fetched from HBM by the first
+// of them is still in L2 when the last one reads it.  Resident-unknown pairs
+// use 40 tiles; dual-tile pairs size the window in bytes (all slices' windows
+// within 48 MB of L2: C4, 20 stages per tile, gets 2 tiles -- with the 40-tile
+// window of round 1 the two C4 groups re-read 1.75x the 51 GB image from HBM).
+// A lone unknown group has no peers and is not paced (round 2 found that its
+// pairs waited on their own stale counter: one unknown, 20M knowns, 5.6 ms ->
+// 1.55 ms, HBM-bound).
 constexpr int kDriftTilesMax = 40;
 constexpr int64_t kDriftWindowBytes = 48ll << 20;
 constexpr int kBatch = 32;         // accumulator columns per tcgen05.wait::ld (x8 loads)
@@ -377,6 +387,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     constexpr int UB = Layout<F>::kUnpackedStageBytes;
     constexpr int HB = UB / 2;                 // one half of an image stage
     constexpr int RB = PAIR ? HB : UB;         // bytes this CTA receives per stage
+    constexpr int kImgHalfRows = HB / kImgRowBytes;  // image-map rows per half stage
+    static_assert(!PAIR || HB % kImgRowBytes == 0, "half stage must be whole image-map rows");
     constexpr int PB = Layout<F>::kPackedStageBytes;
     // Dual-tile CTA pairs (streamed A, long profiles): each A stage feeds the
     // MMAs of two known tiles (one per accumulator), halving the A operand's
@@ -437,8 +449,17 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
     const int n_seg = SPARE ? per_spare : 1;
     const int64_t t_main = PAIR && a.n_spare ? a.t_main : n_tiles;
     const int slice = spare ? n_slices : unit % n_slices;  // partial-list slot
-    const int64_t t_begin = spare ? t_main : t_main * slice / n_slices;
-    const int64_t t_end = spare ? n_tiles : t_main * (slice + 1) / n_slices;
+    // A regular unit takes every n_slices-th of the first t_main tiles, starting at
+    // its slice (slices interleaved, so at any moment the units stream neighbouring
+    // tiles spread over every HBM channel; with one contiguous range per slice the
+    // units advanced in lock step through ranges 1/n_slices of the image apart and
+    // camped on the same channels: one unknown group, 20M x 1024 loci, took 5.6 ms
+    // with per-pair finish times from 1.7 to 5.8 ms).  A spare unit takes the
+    // contiguous tail.  Tiles of a unit ascend, as the top-k insertion requires.
+    const int64_t t_first = spare ? t_main : slice;
+    const int64_t t_stride = spare ? 1 : n_slices;
+    const int64_t t_count = spare ? n_tiles - t_main : (t_main > slice ? (t_main - slice + n_slices - 1) / n_slices : 0);
+    auto tile_of = [&](int64_t i) { return t_first + i * t_stride; };
     auto seg_group = [&](int sg) { return spare ? unit * per_spare + sg : unit / n_slices; };
     auto seg_q0 = [&](int sg) { return ((int64_t)seg_group(sg) * (PAIR ? 2 : 1) + rank) * kM; };
 
@@ -450,6 +471,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         for (int i = 0; i < SU; ++i) {
             ptx::mbar_init(&u_full[i], IMG ? 1 : kConvThreads);
             ptx::mbar_init(&u_empty[i], 1);
+            // pairs with bulk-copied halves: this CTA's own half lands on p_full[i]
+            // (the packed ring is unused with an image)
+            if (PAIR) ptx::mbar_init(&p_full[i], 1);
         }
         for (int i = 0; i < kAccBufs; ++i) {
             ptx::mbar_init(&t_full[i], 1);
@@ -498,20 +522,43 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             // HBM once and served to the other groups from L2: the leader's
             // producer publishes its progress and waits (bounded) while it leads
             // the slowest pair of its slice by more than that.
-            int* prog = (PAIR && leader && a.progress && !spare) ? a.progress + (int64_t)slice * a.n_groups : nullptr;
+            // (a lone unknown group has no peers to pace against)
+            int* prog = (PAIR && leader && a.progress && !spare && a.n_groups > 1)
+                            ? a.progress + (int64_t)slice * a.n_groups
+                            : nullptr;
             const int group = seg_group(0);  // drift control: regular units only (one segment)
+            // lane l watches the counter of group l -- every peer group, never this pair's own
+            // (its own published value is stale by a check and would read as a false lead)
+            const bool watch = lane < a.n_groups && lane != group;
             // The peers' counters are loaded at one check and consumed at the next,
             // so their latency never stalls the operand stream.
             int local_t = 0;
             int peer = 0x7FFFFFFF;  // this lane's peer counter, in flight since the last check
+            // L2 prefetch of the same half `pf_tiles` tiles (>= kPrefetchStages stages) ahead:
+            // a known tile read by few unknown groups comes from HBM at every load, and the
+            // operand ring alone keeps too few bytes in flight to cover HBM latency (one
+            // unknown group: 1.6 TB/s).  Within this segment's tiles only.
+            const int64_t pf_tiles = (int64_t)kTileStep * ((kPrefetchStages + n_kst - 1) / n_kst);
+            const bool pf_on = PAIR && a.l2_prefetch;
+            auto prefetch_half = [&](int64_t i, int ks) {  // i: the unit's tile index
+                if (pf_on && i + pf_tiles < t_count)
+                    ptx::tma_prefetch_2d(&tmap, 0, (int)(((tile_of(i + pf_tiles) * n_kst + ks) * 2 + rank) * kImgHalfRows));
+            };
             // this CTA's half of known tile `tile`, stage `ks` (tensor map over the image,
             // box = one half); completion is counted on the leader's barrier, which expects both
-            auto load_half = [&](int64_t tile, int ks, Ring& r) {
+            auto load_half = [&](int64_t i, int ks, Ring& r) {  // i: the unit's tile index
                 producer_wait(a, &u_empty[r.idx], r.phase ^ 1);
                 if (ptx::elect_one()) {
-                    if (leader) ptx::mbar_expect_tx(&u_full[r.idx], 2 * HB);
-                    ptx::tma_load_2d_pair(sU + r.idx * HB, &tmap, ptx::mapa(&u_full[r.idx], 0), 0,
-                                          (int)(((tile * n_kst + ks) * 2 + rank) * (BN / 2)));
+                    if (a.bulk_b) {
+                        ptx::mbar_expect_tx(&p_full[r.idx], HB);
+                        ptx::bulk_load(sU + r.idx * HB, a.image + ((tile_of(i) * n_kst + ks) * 2 + rank) * (int64_t)HB,
+                                       HB, &p_full[r.idx]);
+                    } else {
+                        if (leader) ptx::mbar_expect_tx(&u_full[r.idx], 2 * HB);
+                        ptx::tma_load_2d_pair(sU + r.idx * HB, &tmap, ptx::mapa(&u_full[r.idx], 0), 0,
+                                              (int)(((tile_of(i) * n_kst + ks) * 2 + rank) * kImgHalfRows));
+                    }
+                    prefetch_half(i, ks);
                 }
                 __syncwarp();
                 r.next();
@@ -520,23 +567,33 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             // first 128-B row of this segment's streamed-A stages (warp-uniform, hoisted)
             const int64_t a_row0 = ((int64_t)seg_group(sg) * 2 + rank) * n_kst * (AB / 128);
             int next_check = 0;
-            for (int64_t t = t_begin; t < t_end; t += kTileStep) {
-                // dual-tile pairs (streamed A): tiles t and t + 1 share every A stage
-                const bool two = kDual && t + 1 < t_end;
+            for (int64_t i = 0; i < t_count; i += kTileStep) {
+                const int64_t t = tile_of(i);
+                // dual-tile pairs (streamed A): the unit's tiles i and i + 1 share every A stage
+                const bool two = kDual && i + 1 < t_count;
                 if (prog && local_t >= next_check) {
                     next_check = local_t + a.drift_every;
+                    // `peer` was loaded at the previous check, drift_every tiles ago: peers in
+                    // step have advanced about that much since, so only a lead beyond the window
+                    // plus that staleness is real -- then wait on fresh reads.  (Waiting on the
+                    // stale lead alone cost a sleep + reload per check: 2 groups x 20M x 1024
+                    // loci took 4.8 ms with a 13-tile window, 11.2 ms with 6, 3.2 ms unpaced.)
                     int lo = __reduce_min_sync(0xFFFFFFFFu, peer);
                     int spin = 0;
-                    for (; spin < 4096 && local_t - lo > a.drift_tiles; ++spin) {
-                        __nanosleep(256);
-                        lo = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
+                    if (local_t - lo > a.drift_tiles + a.drift_every) {
+                        lo = watch ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
                         lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+                        for (; spin < 4096 && local_t - lo > a.drift_tiles; ++spin) {
+                            __nanosleep(256);
+                            lo = watch ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
+                            lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+                        }
                     }
                     if (lane == 0) ptx::st_relaxed(prog + group, spin == 4096 ? 0x7FFFFFFF : local_t);
                     // a peer that stays ~1 ms behind is not co-resident (a shared GPU):
                     // stop pacing rather than wait on it again
                     if (spin == 4096) prog = nullptr;
-                    if (prog) peer = lane < a.n_groups ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
+                    if (prog) peer = watch ? ptx::ld_relaxed(prog + lane) : 0x7FFFFFFF;
                 }
                 if constexpr (kDual) {
                     // A stage ks and the first tile's half at step ks; the second tile's
@@ -553,9 +610,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                             }
                             __syncwarp();
                             ra.next();
-                            load_half(t, ks, ru);
+                            load_half(i, ks, ru);
                         }
-                        if (two && ks >= d) load_half(t + 1, ks - d, ru);
+                        if (two && ks >= d) load_half(i + 1, ks - d, ru);
                     }
                 } else {
                 for (int ks = 0; ks < n_kst; ++ks, rp.next()) {
@@ -586,10 +643,16 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         if (ptx::elect_one()) {
                             if (experiment(a, 4)) {  // timing experiment: no operand traffic
                                 if (leader) ptx::mbar_arrive(&u_full[ru.idx]);
+                            } else if (a.bulk_b) {
+                                ptx::mbar_expect_tx(&p_full[ru.idx], HB);
+                                ptx::bulk_load(sU + ru.idx * HB, a.image + ((t * n_kst + ks) * 2 + rank) * (int64_t)HB, HB,
+                                               &p_full[ru.idx]);
+                                prefetch_half(i, ks);
                             } else {
                                 if (leader) ptx::mbar_expect_tx(&u_full[ru.idx], 2 * HB);
                                 ptx::tma_load_2d_pair(sU + ru.idx * HB, &tmap, ptx::mapa(&u_full[ru.idx], 0), 0,
-                                                      (int)(((t * n_kst + ks) * 2 + rank) * (BN / 2)));
+                                                      (int)(((t * n_kst + ks) * 2 + rank) * kImgHalfRows));
+                                prefetch_half(i, ks);
                             }
                         }
                         __syncwarp();
@@ -635,6 +698,16 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(sU), kBRows * 16, 128);
             Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
+            // stage s of the operand ring is complete: one barrier, or with bulk-copied
+            // pair halves this CTA's own half plus the peer's forwarded arrival
+            auto wait_b = [&](int s, uint32_t phase) {
+                if (PAIR && a.bulk_b) {
+                    ptx::mbar_wait(&p_full[s], phase);
+                    ptx::mbar_wait_cluster(&u_full[s], phase);
+                } else {
+                    ptx::mbar_wait(&u_full[s], phase);
+                }
+            };
             for (int sg = 0; sg < n_seg; ++sg) {
             if (!SA) {  // this segment's resident unknowns are built (phase sg of a_full)
                 if (PAIR)
@@ -643,8 +716,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     ptx::mbar_wait(a_full, (uint32_t)sg & 1u);
             }
             ptx::tc_fence_after();
-            for (int64_t t = t_begin; t < t_end; t += kTileStep) {
-                const bool two = kDual && t + 1 < t_end;
+            for (int64_t i = 0; i < t_count; i += kTileStep) {
+                const bool two = kDual && i + 1 < t_count;
                 const int acc = local % kAccBufs;
                 const uint32_t use = (uint32_t)(local / kAccBufs) & 1u;  // parity of this buffer's use
                 // the second tile of a dual step: the other accumulator
@@ -666,7 +739,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     Ring ay = ra;
                     auto mma_half = [&](uint32_t dacc, int sa, int ks, bool release_a) {
                         const int s = ru.idx;
-                        ptx::mbar_wait(&u_full[s], ru.phase);
+                        wait_b(s, ru.phase);
                         ptx::tc_fence_after();
                         const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)sa * AB) >> 4);
                         const uint64_t bd = b_desc0 + (uint64_t)(((uint32_t)s * RB) >> 4);
@@ -705,7 +778,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
                     const bool trs = tr && experiment(a, 8) && ks < 16;
                     if (trs) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ks] = clock64();
-                    ptx::mbar_wait(&u_full[s], ru.phase);
+                    wait_b(s, ru.phase);
                     if (trs) trace_buf(a)[local * kTrSlots + kTrB0Done + ks] = clock64();
                     ptx::tc_fence_after();
                     // descriptors of this stage's first K-step; later steps add fixed strides
@@ -746,6 +819,16 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 if (tr) trace_buf(a)[local * kTrSlots + kTrMmaIssued] = clock64();
                 local += two ? 2 : 1;
             }
+            }
+        } else if (PAIR && a.bulk_b) {
+            // the peer CTA's MMA warp (idle in a pair) forwards each completed half of
+            // this CTA's ring, in ring order, to the leader's stage barrier
+            Ring rf(SU);
+            const int64_t stages = (int64_t)n_seg * t_count * n_kst;
+            for (int64_t n = 0; n < stages; ++n, rf.next()) {
+                ptx::mbar_wait(&p_full[rf.idx], rf.phase);
+                if (lane == 0) ptx::mbar_arrive_cluster_release(ptx::mapa(&u_full[rf.idx], 0));
+                __syncwarp();
             }
         }
     } else {
@@ -797,7 +880,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         constexpr int kUnits = 2 * BN;
         constexpr int kUnitsPerThread = kConvThreads ? (kUnits + kConvThreads - 1) / (kConvThreads ? kConvThreads : 1) : 1;
         Ring rp(SP), ru(SU);
-        for (int64_t t = t_begin; t < t_end; ++t) {
+        for (int64_t i = 0; i < t_count; ++i) {
             for (int ks = 0; ks < n_kst; ++ks, rp.next(), ru.next()) {
                 const int sp = rp.idx;
                 const int su = ru.idx;
@@ -898,7 +981,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < kAccBufs; ++i) t_empty_leader[i] = ptx::mapa(&t_empty[i], 0);
         }
-        for (int64_t t = t_begin; t < t_end; ++t, ++local) {
+        for (int64_t i = 0; i < t_count; ++i, ++local) {
+            const int64_t t = tile_of(i);
             const int acc = local % kAccBufs;
             // the shared bound is read before the wait so its latency hides behind it
             const uint32_t shared_bound = share ? __ldcg(a.bound + q) : 0xFFFFFFFFu;
@@ -1334,11 +1418,11 @@ int make_image_map(CUtensorMap* map, const CompareArgs& a) {
     if (!fn) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     const Layout<F> lay(a.stride, false, true);
     const int64_t bytes = ceil_div(a.n_refs, Fmt<F>::BN) * lay.n_kst * Layout<F>::kUnpackedStageBytes;
-    cuuint64_t dims[2] = {128, (cuuint64_t)(bytes / 128)};
-    cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {128, (cuuint32_t)(Layout<F>::kUnpackedStageBytes / 2 / 128)};
+    cuuint64_t dims[2] = {kImgRowBytes / 8, (cuuint64_t)(bytes / kImgRowBytes)};
+    cuuint64_t strides[1] = {kImgRowBytes};
+    cuuint32_t box[2] = {kImgRowBytes / 8, (cuuint32_t)(Layout<F>::kUnpackedStageBytes / 2 / kImgRowBytes)};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a.image, dims, strides, box, estr,
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)a.image, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) FASTID_FAIL(FASTID_E_CUDA, "cuTensorMapEncodeTiled (image) failed (%d)", (int)r);
@@ -1447,14 +1531,25 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
         ap.t_main = sp.t_main;
         ap.progress = nullptr;
         {
+            // Resident unknowns (short tiles): a 40-tile window (on-box A/B at 1024 loci: C3
+            // 10.2 ms at 40 tiles vs 12.4 at 20 and 10.8 at 80; 512 unknowns 3.1 ms at 40 vs
+            // 4.1 at the 13 tiles of the byte budget).  Dual-tile pairs (long tiles): the
+            // byte budget (C4: 2 tiles, 16.1 ms vs 17.9 at 3 and 19.0 at 6).
             const int64_t window = kDriftWindowBytes / ((int64_t)n_slices * lay.n_kst * Layout<F>::kUnpackedStageBytes);
-            ap.drift_tiles = (int)std::min<int64_t>(kDriftTilesMax, std::max<int64_t>(2, window));
+            ap.drift_tiles = SA ? (int)std::min<int64_t>(kDriftTilesMax, std::max<int64_t>(2, window)) : kDriftTilesMax;
+            // L2 prefetch of the known-tile stream: off by default (it cost C3 / C4 power and
+            // clock for ~1% on one unknown group); FASTID_L2_PREFETCH=1 turns it on
+            ap.l2_prefetch = 0;
+            if (const char* e = getenv("FASTID_L2_PREFETCH")) ap.l2_prefetch = atoi(e) != 0;
+            ap.bulk_b = 0;  // FASTID_BULK_B=1: 1-D bulk copies per half + peer forwarding
+            if (const char* e = getenv("FASTID_BULK_B")) ap.bulk_b = atoi(e) != 0;
             ap.dual_lag = -1;  // FASTID_DUAL_LAG: stages the second tile of a dual step lags
             if (const char* e = getenv("FASTID_DUAL_LAG")) ap.dual_lag = atoi(e);
-#ifdef FASTID_EXPERIMENTS
+            // FASTID_DRIFT_TILES: the drift window in tiles (scheduling only)
             if (const char* e = getenv("FASTID_DRIFT_TILES")) ap.drift_tiles = std::max(1, atoi(e));
-#endif
-            ap.drift_every = std::max(1, std::min(8, ap.drift_tiles / 4));
+            // checks at least 16 stages apart: a check consumes the peers' counters loaded at
+            // the previous one, and a shorter gap stalls the producer on that load
+            ap.drift_every = std::max(std::max(1, ap.drift_tiles / 4), (int)ceil_div(16, lay.n_kst));
         }
         // drift control only among co-resident pairs, and only for runs long enough to
         // drift (a small comparison skips the counters' memset launch)

@@ -67,6 +67,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// Prefetch one tensor-map box into L2 (no shared-memory destination, no
+// barrier): a later TMA load of the same box then hits in L2.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(x), "r"(y)
+                 : "memory");
+}
+
 // 1-D bulk copy global -> shared, completing `bytes` of transaction on `bar`.
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -146,6 +153,12 @@ __device__ __forceinline__ void cluster_sync() {
 // fence every prior global store of the thread).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+// Arrive with cluster-scope release: orders this thread's earlier observations
+// (e.g. the completion of a bulk copy into its CTA's shared memory) before the
+// arrival seen by a waiter in the peer CTA.
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
 // Wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
