@@ -49,12 +49,17 @@ constexpr int kMaxPackedStages = 12;
 constexpr int kMinPackedStages = 4;
 constexpr int kMaxUnpackedStages = 12;  // barrier slots; dual-tile pairs use up to 12 ring stages
 constexpr int kDefaultUnpackedStages = 8;
-// Dual-tile pairs: the second tile lags the first by kDualLag stages, and the
-// A ring keeps kDualPrefetch stages of prefetch beyond the lag (A stages are
-// L2 reads; fewer than 3 in flight stall the MMA).  A/B on one box
-// (tools/dual_ab.py, C4): A ring 7 / lag 3 reaches 13.2 ms at full clock vs
-// 13.4 ms without a lag; A ring 6 / lag 4 (prefetch 1) 18.7 ms.
-constexpr int kDualLag = 3;
+// Dual-tile pairs: the second tile may lag the first by kDualLag stages (the
+// first tile's accumulator then drains while the second finishes), and the A
+// ring keeps kDualPrefetch stages of prefetch beyond the lag (fewer than 3 A
+// stages in flight stall the MMA: A ring 6 / lag 4 took 18.7 ms on C4).  The
+// lag removes the MMA warp's accumulator wait (1850 -> 75 cycles per step,
+// tools/trace_dual.py) but not time: timed by ncu at equal clocks
+// (tools/ncu_ab.py, 512 x 20M x 5000) A ring 5 / lag 0 takes 13.13-13.15 ms,
+// 4 / 0 13.28, 7 / 0 13.17, 6 / 2 13.26, 7 / 3 13.32-13.34 -- so no lag by
+// default (FASTID_DUAL_LAG / FASTID_DUAL_SA override).
+constexpr int kDualLag = 0;
+constexpr int kDualPrefetch = 4;
 constexpr int kPrefetchStages = 16;
 // The image is read by 2-D TMA boxes over a view of 2 KB rows (u64 elements, the
 // widest inner box): a half stage (12 KB) is 6 rows.  With 128-B rows (96 per
@@ -62,7 +67,6 @@ constexpr int kPrefetchStages = 16;
 // unknown group: 5.6 ms for 20M x 1024 loci); the single-CTA kernel's 1-D bulk
 // copies reach 6.1 TB/s on the same stream.
 constexpr int kImgRowBytes = 2048;  // L2 prefetch distance of the pair kernels' known-tile stream
-constexpr int kDualPrefetch = 3;
 constexpr int kMaxAStages = 8;
 // Warp roles.  The two single-thread issuers (TMA producer, MMA) take the
 // highest warp ids (the scheduler favours higher ids), converters the lowest.
