@@ -156,7 +156,6 @@ struct CompareArgs {
     int dual_lag;     // dual-tile pairs: stages the second tile lags the first (-1 = default)
     int dual_sa;      // dual-tile pairs: A ring depth (0 = default)
     int l2_prefetch;  // pair kernels: L2-prefetch the known-tile stream ahead of the TMA loads
-    int bulk_b;       // pair kernels: each CTA bulk-copies its half into its own barrier, the peer forwards
     int tma_out;  // full matrix through TMA tensor stores: 1 per-warp blocks, 2 per-split blocks (set by the launcher)
     // CTA-pair kernel: spare pairs and the tiles the regular slices cover (the rest go to spares)
     int n_spare;

@@ -475,9 +475,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         for (int i = 0; i < SU; ++i) {
             ptx::mbar_init(&u_full[i], IMG ? 1 : kConvThreads);
             ptx::mbar_init(&u_empty[i], 1);
-            // pairs with bulk-copied halves: this CTA's own half lands on p_full[i]
-            // (the packed ring is unused with an image)
-            if (PAIR) ptx::mbar_init(&p_full[i], 1);
         }
         for (int i = 0; i < kAccBufs; ++i) {
             ptx::mbar_init(&t_full[i], 1);
@@ -553,15 +550,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             auto load_half = [&](int64_t i, int ks, Ring& r) {  // i: the unit's tile index
                 producer_wait(a, &u_empty[r.idx], r.phase ^ 1);
                 if (ptx::elect_one()) {
-                    if (a.bulk_b) {
-                        ptx::mbar_expect_tx(&p_full[r.idx], HB);
-                        ptx::bulk_load(sU + r.idx * HB, a.image + ((tile_of(i) * n_kst + ks) * 2 + rank) * (int64_t)HB,
-                                       HB, &p_full[r.idx]);
-                    } else {
-                        if (leader) ptx::mbar_expect_tx(&u_full[r.idx], 2 * HB);
-                        ptx::tma_load_2d_pair(sU + r.idx * HB, &tmap, ptx::mapa(&u_full[r.idx], 0), 0,
-                                              (int)(((tile_of(i) * n_kst + ks) * 2 + rank) * kImgHalfRows));
-                    }
+                    if (leader) ptx::mbar_expect_tx(&u_full[r.idx], 2 * HB);
+                    ptx::tma_load_2d_pair(sU + r.idx * HB, &tmap, ptx::mapa(&u_full[r.idx], 0), 0,
+                                          (int)(((tile_of(i) * n_kst + ks) * 2 + rank) * kImgHalfRows));
                     prefetch_half(i, ks);
                 }
                 __syncwarp();
@@ -647,11 +638,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         if (ptx::elect_one()) {
                             if (experiment(a, 4)) {  // timing experiment: no operand traffic
                                 if (leader) ptx::mbar_arrive(&u_full[ru.idx]);
-                            } else if (a.bulk_b) {
-                                ptx::mbar_expect_tx(&p_full[ru.idx], HB);
-                                ptx::bulk_load(sU + ru.idx * HB, a.image + ((t * n_kst + ks) * 2 + rank) * (int64_t)HB, HB,
-                                               &p_full[ru.idx]);
-                                prefetch_half(i, ks);
                             } else {
                                 if (leader) ptx::mbar_expect_tx(&u_full[ru.idx], 2 * HB);
                                 ptx::tma_load_2d_pair(sU + ru.idx * HB, &tmap, ptx::mapa(&u_full[ru.idx], 0), 0,
@@ -702,16 +688,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_u32(sU), kBRows * 16, 128);
             Ring ru(SU), ra(SA ? lay.sa : 1);
             int local = 0;
-            // stage s of the operand ring is complete: one barrier, or with bulk-copied
-            // pair halves this CTA's own half plus the peer's forwarded arrival
-            auto wait_b = [&](int s, uint32_t phase) {
-                if (PAIR && a.bulk_b) {
-                    ptx::mbar_wait(&p_full[s], phase);
-                    ptx::mbar_wait_cluster(&u_full[s], phase);
-                } else {
-                    ptx::mbar_wait(&u_full[s], phase);
-                }
-            };
             for (int sg = 0; sg < n_seg; ++sg) {
             if (!SA) {  // this segment's resident unknowns are built (phase sg of a_full)
                 if (PAIR)
@@ -743,7 +719,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     Ring ay = ra;
                     auto mma_half = [&](uint32_t dacc, int sa, int ks, bool release_a) {
                         const int s = ru.idx;
-                        wait_b(s, ru.phase);
+                        ptx::mbar_wait(&u_full[s], ru.phase);
                         ptx::tc_fence_after();
                         const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)sa * AB) >> 4);
                         const uint64_t bd = b_desc0 + (uint64_t)(((uint32_t)s * RB) >> 4);
@@ -782,7 +758,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     if (SA) ptx::mbar_wait(&ar_full[sa], ra.phase);
                     const bool trs = tr && experiment(a, 8) && ks < 16;
                     if (trs) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ks] = clock64();
-                    wait_b(s, ru.phase);
+                    ptx::mbar_wait(&u_full[s], ru.phase);
                     if (trs) trace_buf(a)[local * kTrSlots + kTrB0Done + ks] = clock64();
                     ptx::tc_fence_after();
                     // descriptors of this stage's first K-step; later steps add fixed strides
@@ -823,16 +799,6 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 if (tr) trace_buf(a)[local * kTrSlots + kTrMmaIssued] = clock64();
                 local += two ? 2 : 1;
             }
-            }
-        } else if (PAIR && a.bulk_b) {
-            // the peer CTA's MMA warp (idle in a pair) forwards each completed half of
-            // this CTA's ring, in ring order, to the leader's stage barrier
-            Ring rf(SU);
-            const int64_t stages = (int64_t)n_seg * t_count * n_kst;
-            for (int64_t n = 0; n < stages; ++n, rf.next()) {
-                ptx::mbar_wait(&p_full[rf.idx], rf.phase);
-                if (lane == 0) ptx::mbar_arrive_cluster_release(ptx::mapa(&u_full[rf.idx], 0));
-                __syncwarp();
             }
         }
     } else {
@@ -1545,8 +1511,6 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
             // clock for ~1% on one unknown group); FASTID_L2_PREFETCH=1 turns it on
             ap.l2_prefetch = 0;
             if (const char* e = getenv("FASTID_L2_PREFETCH")) ap.l2_prefetch = atoi(e) != 0;
-            ap.bulk_b = 0;  // FASTID_BULK_B=1: 1-D bulk copies per half + peer forwarding
-            if (const char* e = getenv("FASTID_BULK_B")) ap.bulk_b = atoi(e) != 0;
             ap.dual_lag = -1;  // FASTID_DUAL_LAG: stages the second tile of a dual step lags
             if (const char* e = getenv("FASTID_DUAL_LAG")) ap.dual_lag = atoi(e);
             // FASTID_DRIFT_TILES: the drift window in tiles (scheduling only)
