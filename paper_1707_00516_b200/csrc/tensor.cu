@@ -1315,7 +1315,14 @@ inline SparePlan spare_plan(int64_t n_tiles, int64_t groups, int slices, bool di
     if (disabled || spare <= 0 || groups <= 0 || n_tiles < 16 * (slices + 1)) return p;
     while (spare > 1 && groups % spare) --spare;  // a divisor of the group count
     const int64_t per = groups / spare;
-    const int64_t tail = n_tiles / (1 + slices * per);
+    // equal tile counts per pair, scaled by FASTID_SPARE_SHARE percent (tuning knob:
+    // a spare pair re-reads its tail once per group it serves)
+    static const int share = [] {
+        const char* e = getenv("FASTID_SPARE_SHARE");
+        const int v = e ? atoi(e) : 100;
+        return v > 0 && v <= 200 ? v : 100;
+    }();
+    const int64_t tail = n_tiles * share / (100 * (1 + slices * per));
     if (tail < 1) return p;
     p.n_spare = (int)spare;
     p.t_main = n_tiles - tail;
