@@ -22,7 +22,7 @@ import torch
 from .compare import DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device
 from .panel import ThresholdHits, TopKResult
 
-__all__ = ["KnownDatabase", "PreparedImage", "QueryStager", "DB_OPTIONS"]
+__all__ = ["KnownDatabase", "PreparedImage", "QueryStager", "GraphedSearch", "DB_OPTIONS"]
 
 # Execution variants of a prepared database (fastid_db_option, include/fastid_b200.h).
 # Each computes the same result; they select among kernel paths.
@@ -109,6 +109,82 @@ class QueryStager:
     @property
     def d2h_bytes(self) -> int:
         return self.host_s.numel() * 4 + self.host_x.numel() * 8
+
+
+class GraphedSearch:
+    """One host-buffer top-k search of a fixed shape captured as a CUDA graph.
+
+    The graph holds the whole step -- pinned host -> device copy of the
+    unknowns, their encode into the row layout, the fused compare + top-k
+    launches (regular and spare CTA-pair grids, joined) and the merge, and the
+    device -> pinned host copy of the lists -- so a repeated query of the same
+    shape costs one graph launch instead of a dozen host-side enqueues (the
+    graphs the task names in place of a tracing compiler).  ``run(words)``
+    copies the words into the pinned input, replays, waits, and returns the
+    lists; the result equals ``KnownDatabase.search_words`` of the same words.
+    Built by ``KnownDatabase.graphed_search``.
+    """
+
+    def __init__(self, db: "KnownDatabase", n_queries: int, k: int, max_score: int | None = None):
+        from . import _native
+
+        self.db, self.n_queries, self.k = db, int(n_queries), int(k)
+        p = db.panel
+        dev = db.device
+        self.stager = QueryStager(self.n_queries, p.n_words, p.word_width, p.bit_length, self.k, dev)
+        st = self.stager
+        with torch.cuda.device(dev):
+            st.workspace = torch.empty(
+                topk_workspace_bytes_for(p.n_profiles, self.n_queries, self.k, db.formulation), dtype=torch.uint8,
+                device=dev)
+            self.stream = torch.cuda.Stream(dev)
+            self.stream.wait_stream(torch.cuda.current_stream(dev))
+            lib = _native.lib()
+
+            def step():
+                cs = torch.cuda.current_stream(dev)
+                st.dev_in.copy_(st.host_in, non_blocking=True)
+                _native.check(lib.fastid_load_words(
+                    st.dev_in.data_ptr(), self.n_queries, st.dev_in.shape[1], st.panel.rows.data_ptr(),
+                    st.panel.stride, cs.cuda_stream), "fastid_load_words")
+                s, x = db.topk_device(st.panel, self.k, max_score, st.workspace, (st.out_s, st.out_x))
+                st.host_s.copy_(s, non_blocking=True)
+                st.host_x.copy_(x, non_blocking=True)
+
+            # warm up on the capture stream (the library keeps launch scratch per stream;
+            # a first use inside the capture would have to allocate), then capture
+            with torch.cuda.stream(self.stream):
+                step()
+            self.stream.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                step()
+
+    def run(self, query_words: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """Top-k of a (n_queries, N_W) host word array through the captured graph."""
+        from .errors import CorruptProfileError, PanelMismatchError
+        from .panel import padding_mask
+
+        p = self.db.panel
+        qw = np.ascontiguousarray(query_words)
+        if qw.dtype.itemsize * 8 != p.word_width or qw.shape != (self.n_queries, p.n_words):
+            raise PanelMismatchError(f"query words {qw.shape}/{qw.dtype} do not match the captured search "
+                                     f"({self.n_queries} x {p.n_words} {p.word_width}-bit words)")
+        mask = padding_mask(p.bit_length, p.word_width)
+        if mask and qw.size and np.any(qw[:, -1] & qw.dtype.type(mask)):
+            raise CorruptProfileError(f"nonzero padding past bit {p.bit_length}")
+        st = self.stager
+        st.host_in.numpy()[:] = qw.view(np.uint8).reshape(self.n_queries, -1)
+        with torch.cuda.stream(self.stream):  # replay() launches on the current stream
+            self.graph.replay()
+        self.stream.synchronize()
+        return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
+
+
+def topk_workspace_bytes_for(n_refs: int, n_queries: int, k: int, formulation) -> int:
+    from .compare import topk_workspace_bytes
+
+    return topk_workspace_bytes(n_refs, n_queries, k, formulation)
 
 
 class KnownDatabase:
@@ -274,6 +350,12 @@ class KnownDatabase:
     def _read_back(st: QueryStager) -> tuple[np.ndarray, np.ndarray]:
         st.done.synchronize()
         return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
+
+    def graphed_search(self, n_queries: int, k: int = 16, max_score: int | None = None) -> GraphedSearch:
+        """Capture the host-buffer top-k of ``n_queries`` unknowns as a CUDA graph
+        (GraphedSearch): for repeated queries of one shape, one graph launch per
+        search."""
+        return GraphedSearch(self, n_queries, k, max_score)
 
     def search(self, queries, k: int = 16, max_score: int | None = None) -> TopKResult:
         """Per unknown, the k closest knowns by (score asc, global index asc)."""

@@ -732,3 +732,30 @@ def test_search_many_pipelined(rng):
         es, ex, _ = oracle.topk(r, q, 8, 0xFFFFFFFE)
         assert np.array_equal(s, es) and np.array_equal(x, ex)
     assert list(db.search_many([], 8)) == []
+
+
+@pytest.mark.parametrize("n_r,n_q,L", [(30_000, 2048, 1024), (9_000, 100, 5000), (500, 1, 1024)])
+def test_graphed_search(rng, n_r, n_q, L):
+    """The host-buffer top-k captured as one CUDA graph (H2D, encode, compare +
+    top-k incl. the spare grid, merge, D2H): replays with new unknowns equal the
+    oracle; wrong shapes and nonzero padding are rejected as search_words does."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    db = KnownDatabase(r, L)
+    g = db.graphed_search(n_q, 16)
+    for _ in range(3):
+        q, _ = rand_words(rng, n_q, nw, 64, L)
+        q[: min(8, n_q)] = r[rng.integers(0, n_r, min(8, n_q))]
+        s, x = g.run(q)
+        es, ex, _ = oracle.topk(r, q, 16, 0xFFFFFFFE)
+        assert np.array_equal(s, es) and np.array_equal(x, ex)
+    with pytest.raises(m.PanelMismatchError):
+        g.run(np.zeros((n_q + 1, nw), np.uint64))
+    if L % 64:
+        bad = np.zeros((n_q, nw), np.uint64)
+        bad[0, -1] = np.uint64(1)
+        with pytest.raises(m.CorruptProfileError):
+            g.run(bad)
