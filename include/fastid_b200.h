@@ -153,6 +153,13 @@ typedef struct fastid_db fastid_db;
 FASTID_API size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation);
 FASTID_API int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride, int64_t bit_length,
                                 int formulation, void* stream, fastid_db** out);
+/* As fastid_db_create, but the image is built into the caller's device buffer
+ * `image` (at least fastid_db_image_bytes(n_refs, bit_length, formulation)
+ * bytes), which the handle does not own or free.  With it a panel whose whole
+ * image does not fit is searched chunk by chunk at the image kernels' speed:
+ * one reusable buffer, a handle per chunk of rows (ref_base = chunk offset). */
+FASTID_API int fastid_db_create_in(const void* refs, int64_t n_refs, int64_t stride, int64_t bit_length,
+                                   int formulation, void* image, size_t image_bytes, void* stream, fastid_db** out);
 FASTID_API int fastid_db_destroy(fastid_db* db);
 FASTID_API int fastid_db_formulation(const fastid_db* db);
 

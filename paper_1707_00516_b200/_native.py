@@ -137,6 +137,7 @@ def _signatures() -> dict:
         "fastid_parsed_panel_free": ([vp], None),
         "fastid_db_image_bytes": ([i64, i64, i32], sz),
         "fastid_db_create": ([vp, i64, i64, i64, i32, vp, ctypes.POINTER(vp)], i32),
+        "fastid_db_create_in": ([vp, i64, i64, i64, i32, vp, sz, vp, ctypes.POINTER(vp)], i32),
         "fastid_db_destroy": ([vp], i32),
         "fastid_db_formulation": ([vp], i32),
         "fastid_db_set_option": ([vp, i32, i32], i32),

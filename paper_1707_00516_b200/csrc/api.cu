@@ -570,10 +570,11 @@ struct fastid_db {
     const void* refs;
     int64_t n_refs, stride, bit_length;
     int formulation;  // resolved
-    void* image;      // owned; null for the CUDA-core formulation
+    void* image;      // null for the CUDA-core formulation
     size_t image_bytes;
     int device;
-    int options;  // FASTID_OPT_* bits
+    int options;      // FASTID_OPT_* bits
+    bool owns_image;  // false: the caller's buffer (fastid_db_create_in)
 };
 
 extern "C" size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation) {
@@ -588,7 +589,7 @@ extern "C" int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride
     *out = nullptr;
     if (int rc = check_compare(refs, n_refs, refs, 0, stride, bit_length, formulation)) return rc;
     auto* db = new fastid_db{refs, n_refs, stride, bit_length, resolve_formulation(formulation, bit_length),
-                             nullptr, 0, 0, 0};
+                             nullptr, 0, 0, 0, true};
     cudaGetDevice(&db->device);
     if (db->formulation != FASTID_POPC && n_refs > 0) {
         db->image_bytes = tensor_image_bytes(n_refs, bit_length, db->formulation);
@@ -609,9 +610,31 @@ extern "C" int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride
     return FASTID_OK;
 }
 
+extern "C" int fastid_db_create_in(const void* refs, int64_t n_refs, int64_t stride, int64_t bit_length,
+                                   int formulation, void* image, size_t image_bytes, void* stream, fastid_db** out) {
+    if (!out) FASTID_FAIL(FASTID_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (int rc = check_compare(refs, n_refs, refs, 0, stride, bit_length, formulation)) return rc;
+    const int f = resolve_formulation(formulation, bit_length);
+    const size_t need = (f == FASTID_POPC || n_refs == 0) ? 0 : tensor_image_bytes(n_refs, bit_length, f);
+    if (need && (!image || image_bytes < need))
+        FASTID_FAIL(FASTID_E_CAPACITY, "image buffer of %zu bytes is smaller than the %zu required", image_bytes, need);
+    auto* db = new fastid_db{refs, n_refs, stride, bit_length, f, need ? image : nullptr, need, 0, 0, false};
+    cudaGetDevice(&db->device);
+    if (need) {
+        CompareArgs a = make_args(refs, n_refs, refs, 0, stride, bit_length);
+        if (int rc = build_tensor_image(a, f, image, (cudaStream_t)stream)) {
+            delete db;
+            return rc;
+        }
+    }
+    *out = db;
+    return FASTID_OK;
+}
+
 extern "C" int fastid_db_destroy(fastid_db* db) {
     if (!db) return FASTID_OK;
-    if (db->image) {
+    if (db->image && db->owns_image) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(db->device);

@@ -22,7 +22,7 @@ import torch
 from .compare import DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device
 from .panel import ThresholdHits, TopKResult
 
-__all__ = ["KnownDatabase", "PreparedImage", "QueryStager", "GraphedSearch", "DB_OPTIONS"]
+__all__ = ["KnownDatabase", "PreparedImage", "ChunkedImage", "QueryStager", "GraphedSearch", "DB_OPTIONS"]
 
 # Execution variants of a prepared database (fastid_db_option, include/fastid_b200.h).
 # Each computes the same result; they select among kernel paths.
@@ -111,6 +111,89 @@ class QueryStager:
         return self.host_s.numel() * 4 + self.host_x.numel() * 8
 
 
+class ChunkedImage:
+    """The tensor image of a known panel too large for one image in device memory.
+
+    One reusable device buffer holds the image of ``chunk_rows`` rows (a
+    multiple of the 192-row tile); each search builds the chunks' images into
+    it in turn (fastid_db_create_in: an image-build kernel into the caller's
+    buffer, stream-ordered after the previous chunk's comparison) and runs the
+    image kernels per chunk with the chunk's row offset, so a panel whose
+    packed rows fit but whose 4-bit image does not (e.g. 20M x 16384 loci:
+    41 GB packed, 164 GB image) is still searched by the CTA-pair kernels; the
+    chunks' results combine exactly (top-k lists merged with the (score,
+    index) order, full-matrix rows and threshold hits by row range).
+    """
+
+    def __init__(self, panel: DevicePanel, formulation: str | int, chunk_rows: int | None = None):
+        from . import _native
+        from .errors import DeviceError
+
+        L = _native.lib()
+        self.panel = panel
+        code = _native.formulation_code(formulation)
+        if code == 0:  # auto: the tensor formulation that runs this length
+            code = _native.FORMULATIONS["tensor_f4"] if _native.supports("tensor_f4", panel.bit_length) else 1
+        self.code = code
+        tile = 192
+        per_tile = L.fastid_db_image_bytes(tile, panel.bit_length, code)
+        if per_tile == 0:
+            raise DeviceError("formulation has no tensor image")
+        if chunk_rows is None:
+            free = torch.cuda.mem_get_info(panel.device)[0]
+            chunk_rows = int(free * 0.6) // per_tile * tile
+        chunk_rows = min(int(chunk_rows) // tile * tile, -(-panel.n_profiles // tile) * tile)
+        if chunk_rows < tile:
+            raise DeviceError(f"cannot allocate even one {tile}-row chunk of the tensor image")
+        self.chunk_rows = chunk_rows
+        self.buf = torch.empty(L.fastid_db_image_bytes(chunk_rows, panel.bit_length, code), dtype=torch.uint8,
+                               device=panel.device)
+        self.options = 0
+
+    def set_option(self, name: str, enabled: bool = True) -> None:
+        if name not in DB_OPTIONS:
+            raise ValueError(f"option must be one of {sorted(DB_OPTIONS)}, got {name!r}")
+        self.options = (self.options | DB_OPTIONS[name]) if enabled else (self.options & ~DB_OPTIONS[name])
+
+    def chunks(self):
+        """(first row, rows, the chunk's prepared image) per chunk, in row order; each
+        image is built on the current stream into the shared buffer."""
+        from . import _native
+
+        L = _native.lib()
+        n = self.panel.n_profiles
+        for r0 in range(0, n, self.chunk_rows):
+            nr = min(self.chunk_rows, n - r0)
+            sub = self.panel.slice(r0, r0 + nr)
+            h = ctypes.c_void_p()
+            with torch.cuda.device(self.panel.device):
+                _native.check(L.fastid_db_create_in(
+                    sub.rows.data_ptr(), nr, sub.stride, sub.bit_length, self.code, self.buf.data_ptr(),
+                    self.buf.numel(), torch.cuda.current_stream(self.panel.device).cuda_stream, ctypes.byref(h)),
+                    "fastid_db_create_in")
+            for name, bit in DB_OPTIONS.items():
+                if self.options & bit:
+                    _native.check(L.fastid_db_set_option(h, bit, 1), "fastid_db_set_option")
+            view = _ChunkView(h)
+            try:
+                yield r0, nr, sub, view
+            finally:
+                L.fastid_db_destroy(h)  # the handle is host state only; kernels already enqueued
+
+
+# Below this many unknowns a chunked image costs more to build per search than it
+# saves: 20M x 16384 loci, top-16 (tools/chunked_vs_packed.py): 64 unknowns 72 ms
+# chunked vs 20 ms packed, 512: 101 vs 75, 1024: 139 vs 152, 2048: 226 vs 306.
+CHUNKED_IMAGE_MIN_QUERIES = 1024
+
+
+class _ChunkView:
+    """A chunk's fastid_db handle, shaped like PreparedImage for the compare helpers."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+
 class GraphedSearch:
     """One host-buffer top-k search of a fixed shape captured as a CUDA graph.
 
@@ -191,7 +274,7 @@ class KnownDatabase:
     """A known panel resident on one device (or one shard of it, ``ref_base`` = global offset)."""
 
     def __init__(self, refs, bit_length: int | None = None, device=None, ref_base: int = 0,
-                 formulation: str | int = "auto", prepare: bool = True):
+                 formulation: str | int = "auto", prepare: bool = True, image_chunk_rows: int | None = None):
         self.device = _require_cuda(device)
         if isinstance(refs, DevicePanel):
             self.panel = refs
@@ -208,8 +291,12 @@ class KnownDatabase:
         # database whose image does not fit in device memory (4 bits per locus for
         # mxf4) keeps only its packed rows and runs the unpacking kernels instead
         self.image = None
+        self.chunked_min_queries = CHUNKED_IMAGE_MIN_QUERIES
         if prepare and self.panel.n_profiles:
-            self.image = self._prepare(formulation)
+            # image_chunk_rows: build the image chunk by chunk into one buffer of that
+            # many rows (what a panel whose whole image does not fit falls back to)
+            self.image = (ChunkedImage(self.panel, formulation, image_chunk_rows) if image_chunk_rows
+                          else self._prepare(formulation))
 
     def _prepare(self, formulation):
         from .errors import DeviceError
@@ -223,10 +310,13 @@ class KnownDatabase:
                 if attempt == 0:
                     torch.cuda.empty_cache()  # cached torch blocks may be what is missing
                     continue
-                import warnings
+                try:
+                    return ChunkedImage(self.panel, formulation)
+                except DeviceError as e2:
+                    import warnings
 
-                warnings.warn(f"tensor image does not fit on {self.device} ({e}); using packed operands",
-                              RuntimeWarning, stacklevel=3)
+                    warnings.warn(f"tensor image does not fit on {self.device} ({e}; {e2}); using packed operands",
+                                  RuntimeWarning, stacklevel=3)
         return None
 
     def set_option(self, name: str, enabled: bool = True) -> None:
@@ -249,13 +339,62 @@ class KnownDatabase:
         return DevicePanel.from_panel(queries, self.device)
 
     # -- device-resident calls (inputs already in HBM) -------------------------
+    def _chunked_for(self, n_queries: int) -> bool:
+        """Whether a batch this size goes through the chunked image (large batches) or
+        the packed-operand kernels (small ones), when the whole image did not fit."""
+        return isinstance(self.image, ChunkedImage) and n_queries >= self.chunked_min_queries
+
+    def _plain_image(self):
+        return None if isinstance(self.image, ChunkedImage) else self.image
+
     def topk_device(self, queries: DevicePanel, k: int, max_score: int | None = None, workspace=None, out=None,
                     events=None):
+        if self._chunked_for(queries.n_profiles):
+            return self._topk_chunked(queries, k, max_score, workspace, out)
         return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out,
-                           events=events, image=self.image)
+                           events=events, image=self._plain_image())
+
+    def _topk_chunked(self, queries: DevicePanel, k: int, max_score, workspace, out):
+        """Per chunk: its image, the fused top-k with the chunk's row offset, and a merge
+        of the chunk's lists into the running lists (two-list fastid_merge_topk)."""
+        from . import _native
+
+        n_q = queries.n_profiles
+        dev = self.device
+        if out is None:
+            out = (torch.empty((n_q, k), dtype=torch.int32, device=dev),
+                   torch.empty((n_q, k), dtype=torch.int64, device=dev))
+        s, x = out
+        if n_q == 0:
+            return s, x
+        cand_s = torch.empty((2, n_q, k), dtype=torch.int32, device=dev)
+        cand_x = torch.empty((2, n_q, k), dtype=torch.int64, device=dev)
+        L = _native.lib()
+        first = True
+        for r0, nr, sub, view in self.image.chunks():
+            dst = (cand_s[0], cand_x[0]) if first else (cand_s[1], cand_x[1])
+            topk_device(sub, queries, k, max_score, self.ref_base + r0, self.formulation, workspace, dst, image=view)
+            if not first:
+                with torch.cuda.device(dev):
+                    _native.check(L.fastid_merge_topk(cand_s.data_ptr(), cand_x.data_ptr(), 2, n_q, k, k,
+                                                      s.data_ptr(), x.data_ptr(),
+                                                      torch.cuda.current_stream(dev).cuda_stream),
+                                  "fastid_merge_topk")
+                cand_s[0].copy_(s)
+                cand_x[0].copy_(x)
+            first = False
+        s.copy_(cand_s[0])
+        x.copy_(cand_x[0])
+        return s, x
 
     def full_device(self, queries: DevicePanel, out=None) -> torch.Tensor:
-        return compare_device(self.panel, queries, out, self.formulation, image=self.image)
+        if self._chunked_for(queries.n_profiles):
+            if out is None:
+                out = torch.empty((self.panel.n_profiles, queries.n_profiles), dtype=torch.int32, device=self.device)
+            for r0, nr, sub, view in self.image.chunks():
+                compare_device(sub, queries, out[r0:r0 + nr], self.formulation, image=view)
+            return out
+        return compare_device(self.panel, queries, out, self.formulation, image=self._plain_image())
 
     # -- host-buffer public calls ------------------------------------------------
     def stager(self, n_queries: int, k: int, slot: int = 0) -> QueryStager:
@@ -364,5 +503,15 @@ class KnownDatabase:
         return TopKResult(tuple(queries.ids), s, x, self.panel.ids)
 
     def threshold(self, queries, threshold: int, capacity: int | None = None) -> ThresholdHits:
+        n_q = queries.n_profiles if isinstance(queries, DevicePanel) else len(queries.words)
+        if self._chunked_for(n_q):
+            parts = [threshold_hits(sub, queries, threshold, capacity, self.formulation, self.device,
+                                    ref_base=self.ref_base + r0, image=view)
+                     for r0, nr, sub, view in self.image.chunks()]
+            q = np.concatenate([h.query for h in parts])
+            r = np.concatenate([h.ref for h in parts])
+            sc = np.concatenate([h.score for h in parts])
+            order = np.lexsort((r, q))
+            return ThresholdHits(q[order], r[order], sc[order], int(threshold))
         return threshold_hits(self.panel, queries, threshold, capacity, self.formulation, self.device,
-                              ref_base=self.ref_base, image=self.image)
+                              ref_base=self.ref_base, image=self._plain_image())

@@ -759,3 +759,50 @@ def test_graphed_search(rng, n_r, n_q, L):
         bad[0, -1] = np.uint64(1)
         with pytest.raises(m.CorruptProfileError):
             g.run(bad)
+
+
+@pytest.mark.parametrize("n_r,n_q,L,chunk", [(40_000, 300, 1024, 192 * 40), (12_000, 64, 5000, 192 * 9),
+                                             (3_000, 2048, 1024, 192)])
+def test_chunked_image(rng, n_r, n_q, L, chunk):
+    """A panel searched through a chunked tensor image (one reusable image buffer,
+    each chunk built in turn, fastid_db_create_in): top-k, full matrix and
+    threshold hits equal the oracle across chunk boundaries, with a ref_base
+    offset and ties that straddle chunks."""
+    m = fb()
+    from paper_1707_00516_b200.search import ChunkedImage, KnownDatabase
+
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    q, _ = rand_words(rng, n_q, nw, 64, L)
+    q[:20] = r[rng.integers(0, n_r, 20)]
+    r[-2:] = r[:2]
+    db = KnownDatabase(r, L, ref_base=5, image_chunk_rows=chunk)
+    assert isinstance(db.image, ChunkedImage)
+    db.chunked_min_queries = 1  # every batch through the chunks (the default sends small batches packed)
+    for k in (16, 3):
+        s, x = db.search_words(q, k)
+        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE)
+        assert np.array_equal(s, es) and np.array_equal(x, np.where(ex >= 0, ex + 5, -1)), k
+    if n_r * n_q <= 40_000_000:
+        exp = oracle.blocked(r, np.ascontiguousarray(q.T), 64, 16, os.cpu_count() or 1)
+        full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+        assert np.array_equal(full, exp)
+        thr = int(np.percentile(exp[:, :4], 1))
+        hits = db.threshold(m.Panel(tuple(range(n_q)), q, L), thr)
+        hq, hr, hs = oracle.threshold_from_matrix(exp, thr)
+        assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr + 5) and np.array_equal(hits.score, hs)
+
+
+def test_chunked_image_small_batches_use_packed_operands(rng):
+    """Below CHUNKED_IMAGE_MIN_QUERIES a database on a chunked image answers through
+    the packed-operand kernels (cheaper than building every chunk's image): same result."""
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1024
+    r, _ = rand_words(rng, 20_000, 16, 64, L)
+    q, _ = rand_words(rng, 40, 16, 64, L)
+    db = KnownDatabase(r, L, image_chunk_rows=192 * 7)
+    assert not db._chunked_for(40)
+    s, x = db.search_words(q, 8)
+    es, ex, _ = oracle.topk(r, q, 8, 0xFFFFFFFE)
+    assert np.array_equal(s, es) and np.array_equal(x, ex)
