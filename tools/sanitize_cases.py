@@ -77,6 +77,21 @@ def main():
     es, ex, _ = oracle.topk_from_matrix(expected, 8)
     assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), "streamed topk"
     n_cases += 1
+    # chunked tensor image (one reusable buffer, fastid_db_create_in) and a graphed search
+    refs, queries = panel(rng, 3000, 1024, "r"), panel(rng, 90, 1024, "q")
+    expected = oracle.naive(refs.words, queries.words)
+    db = KnownDatabase(refs, image_chunk_rows=192 * 5)
+    db.chunked_min_queries = 1
+    s, x = db.search_words(queries.words, 8)
+    es, ex, _ = oracle.topk_from_matrix(expected, 8)
+    assert np.array_equal(s, es) and np.array_equal(x, ex), "chunked topk"
+    full = db.full_device(fb.DevicePanel.from_panel(queries)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(full, expected), "chunked full"
+    db = KnownDatabase(refs)
+    g = db.graphed_search(90, 8)
+    s, x = g.run(queries.words)
+    assert np.array_equal(s, es) and np.array_equal(x, ex), "graphed topk"
+    n_cases += 3
     torch.cuda.synchronize()
     print(f"sanitize cases ok ({n_cases})")
 
