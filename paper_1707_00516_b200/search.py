@@ -146,8 +146,11 @@ class ChunkedImage:
         if chunk_rows < tile:
             raise DeviceError(f"cannot allocate even one {tile}-row chunk of the tensor image")
         self.chunk_rows = chunk_rows
-        self.buf = torch.empty(L.fastid_db_image_bytes(chunk_rows, panel.bit_length, code), dtype=torch.uint8,
-                               device=panel.device)
+        try:
+            self.buf = torch.empty(L.fastid_db_image_bytes(chunk_rows, panel.bit_length, code), dtype=torch.uint8,
+                                   device=panel.device)
+        except torch.cuda.OutOfMemoryError as e:
+            raise DeviceError(f"cannot allocate a {chunk_rows}-row image chunk: {e}") from None
         self.options = 0
 
     def set_option(self, name: str, enabled: bool = True) -> None:
