@@ -151,12 +151,17 @@ class ChunkedImage:
                                    device=panel.device)
         except torch.cuda.OutOfMemoryError as e:
             raise DeviceError(f"cannot allocate a {chunk_rows}-row image chunk: {e}") from None
-        self.options = 0
+        self._bits = 0
 
     def set_option(self, name: str, enabled: bool = True) -> None:
+        """Switch one DB_OPTIONS execution variant for every chunk's handle."""
         if name not in DB_OPTIONS:
             raise ValueError(f"option must be one of {sorted(DB_OPTIONS)}, got {name!r}")
-        self.options = (self.options | DB_OPTIONS[name]) if enabled else (self.options & ~DB_OPTIONS[name])
+        self._bits = (self._bits | DB_OPTIONS[name]) if enabled else (self._bits & ~DB_OPTIONS[name])
+
+    @property
+    def options(self) -> set:
+        return {n for n, b in DB_OPTIONS.items() if self._bits & b}
 
     def chunks(self):
         """(first row, rows, the chunk's prepared image) per chunk, in row order; each
@@ -175,7 +180,7 @@ class ChunkedImage:
                     self.buf.numel(), torch.cuda.current_stream(self.panel.device).cuda_stream, ctypes.byref(h)),
                     "fastid_db_create_in")
             for name, bit in DB_OPTIONS.items():
-                if self.options & bit:
+                if self._bits & bit:
                     _native.check(L.fastid_db_set_option(h, bit, 1), "fastid_db_set_option")
             view = _ChunkView(h)
             try:
