@@ -65,7 +65,23 @@ def case(seed):
     for name in DB_OPTIONS:
         if rng.random() < 0.15:
             db.set_option(name, True)
-    mode = rng.choice(["topk", "topk", "threshold", "full"])
+    mode = rng.choice(["topk", "topk", "threshold", "full", "streamed", "graphed"])
+    if mode == "streamed":  # host panel streamed through the device in random chunks
+        k = int(rng.integers(1, 33))
+        cr = int(rng.integers(1, n_r + 1)) if rng.random() < 0.8 else 0
+        R = m.Panel(tuple(range(n_r)), r, L)
+        Q = m.Panel(tuple(range(n_q)), q, L)
+        res = m.topk_streamed(R, Q, k, formulation=form, chunk_rows=cr, ref_base=7)
+        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE, workers)
+        ok = np.array_equal(res.scores, es) and np.array_equal(res.index, np.where(ex >= 0, ex + 7, -1))
+        return ok, f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} streamed chunk_rows={cr} k={k}"
+    if mode == "graphed":
+        k = int(rng.integers(1, 33))
+        g = db.graphed_search(n_q, k)
+        s, x = g.run(q)
+        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE, workers)
+        ok = np.array_equal(s, es) and np.array_equal(x, np.where(ex >= 0, ex + db.ref_base, -1))
+        return ok, f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} chunk={chunk} graphed k={k}"
     desc = f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} chunk={chunk} opts={sorted(getattr(db.image, 'options', set()) or [])} {mode}"
     base = db.ref_base
     if mode == "topk":
