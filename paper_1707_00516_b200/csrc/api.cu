@@ -471,7 +471,12 @@ int topk_partials_impl(const void* refs, const void* image, int options, int64_t
     if (workspace_bytes < need)
         FASTID_FAIL(FASTID_E_CAPACITY, "workspace of %zu bytes is smaller than the %zu required", workspace_bytes,
                     need);
-    const int f = resolve_formulation(formulation, bit_length);
+    // auto, packed rows, a handful of unknowns: the CUDA-core scan reads the packed
+    // rows once and beats the tensor kernels there (20M x 1024 loci, top-16:
+    // 1 unknown 0.70 vs 1.52 ms, 4: 1.41 vs 1.54, 8: 2.41 vs 1.55; popc.cu)
+    const int f = (formulation == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
+                      ? FASTID_POPC
+                      : resolve_formulation(formulation, bit_length);
     const int kp = list_size_for(k);
     const int parts = parts_for(f, n_refs, n_queries);
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);

@@ -43,6 +43,7 @@ void note_launch();
 
 constexpr int kMaxTopK = 32;
 constexpr int kMaxMergeLists = 768;  // candidate lists one merge folds per unknown (merge.cu)
+constexpr int kScanAutoMaxQueries = 4;  // auto top-k on packed rows: the CUDA-core scan up to this many unknowns
 constexpr int kMinSlots = 32;  // lists per unknown that publish their best value (shared top-k bound)
 constexpr uint32_t kEmptyScore = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyLocal = 0xFFFFFFFFu;

@@ -174,6 +174,202 @@ __global__ void __launch_bounds__(kThreads, MODE == kTopK ? 1 : 2) popc_kernel(C
     }
 }
 
+// ---- few unknowns: a streaming scan (the single-profile search) ---------------
+//
+// With a handful of unknowns the 128 x 128 tile above wastes almost all of its
+// POPC work on empty unknown rows (one unknown vs 20M knowns: 28 ms), and the
+// tensor kernels stream the whole 4-bit image (1.5 ms).  The scan reads each
+// packed known row once (2.56 GB for 20M x 1024 loci) against up to
+// kScanMaxQ complemented unknowns held in shared memory.  A warp scores 32
+// rows per step, one per lane; the per-unknown state is sized to the batch
+// (QN) so a single profile runs at high occupancy with many rows in flight,
+// and the rows arrive by coalesced loads (four whole rows per instruction)
+// through a small per-warp staging tile.  (Eight lanes per row with
+// shuffle-summed partial counts, double-buffered cp.async staging and a
+// register prefetch of the next step all measured slower for one unknown
+// against 20M x 1024 loci: 2.7, 1.8 and 2.3 ms.)  Per unknown the
+// warp keeps a sorted top-KP list spread over its lanes (lane l holds entry
+// l), admits a row that orders before the list's last entry and whose score is
+// <= the shared bound (a.bound[j]: the smallest KP-th best any warp has
+// published), and inserts with one shuffle round.  At the end the CTA's warps'
+// lists are merged into one partial list per CTA, which the merge kernel folds
+// like any other partials.
+constexpr int kScanMaxQ = 16;
+constexpr int kScanWarps = 8;
+constexpr int kScanPiece = 8;  // uint4 per row per staging round (128 B)
+constexpr int kScanTile16 = 32 * (kScanPiece + 1);  // one warp's staging tile (uint4), padded rows
+
+template <int KP, int QN>
+__global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_kernel(CompareArgs a) {
+    extern __shared__ __align__(16) uint4 sq[];  // [n_queries][n16] complemented unknown rows
+    const int n16 = (int)(a.stride / 16);
+    const int nq = (int)a.n_queries;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint4* tile = sq + nq * n16 + warp * kScanTile16;  // this warp's staging tile
+    for (int i = threadIdx.x; i < nq * n16; i += blockDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(a.queries)[(int64_t)(i / n16) * n16 + i % n16];
+        sq[i] = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
+    }
+    // zero padding in the known rows makes the complemented padding of the
+    // unknowns harmless (r & ~q = 0 past L)
+    __syncthreads();
+    uint32_t ls[QN], lx[QN], ks[QN], kx[QN], gb[QN];
+#pragma unroll
+    for (int j = 0; j < QN; ++j) {
+        ls[j] = kEmptyScore;
+        lx[j] = kEmptyLocal;
+        ks[j] = kEmptyScore;  // the list's KP-th entry (every lane holds a copy)
+        kx[j] = kEmptyLocal;
+        gb[j] = a.max_score;  // admit score <= min(shared bound, cap)
+    }
+    const int64_t warps = (int64_t)gridDim.x * kScanWarps;
+    const int64_t n_steps = (a.n_refs + 31) / 32;
+    int64_t step_no = 0;
+    for (int64_t st = (int64_t)blockIdx.x * kScanWarps + warp; st < n_steps; st += warps, ++step_no) {
+        if ((step_no & 7) == 0) {
+#pragma unroll
+            for (int j = 0; j < QN; ++j)
+                if (j < nq) {
+                    const uint32_t g = __ldcg(a.bound + j);
+                    if (g < gb[j]) gb[j] = g;
+                }
+        }
+        const int64_t r = st * 32 + lane;
+        const bool valid = r < a.n_refs;
+        uint32_t acc[QN];
+#pragma unroll
+        for (int j = 0; j < QN; ++j) acc[j] = 0;
+        // the step's 32 rows, 128 B per row per round: coalesced loads (4 whole rows,
+        // 512 contiguous bytes, per instruction) through this warp's staging tile,
+        // then each lane scores its own row from shared memory
+        const uint8_t* rows0 = a.refs + st * 32 * a.stride;
+        for (int c = 0; c < n16; c += kScanPiece) {
+#pragma unroll
+            for (int i = 0; i < kScanPiece; ++i) {
+                const int p = lane + 32 * i, prow = p / kScanPiece, pcol = c + p % kScanPiece;
+                const bool ok = st * 32 + prow < a.n_refs && pcol < n16;
+                cp_async16(tile + prow * (kScanPiece + 1) + p % kScanPiece,
+                           ok ? rows0 + prow * a.stride + (int64_t)pcol * 16 : a.refs, ok ? 16 : 0);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncwarp();
+#pragma unroll
+            for (int w = 0; w < kScanPiece; ++w) {
+                if (c + w < n16) {
+                    const uint4 rv = tile[lane * (kScanPiece + 1) + w];
+#pragma unroll
+                    for (int j = 0; j < QN; ++j)
+                        if (j < nq) {
+                            const uint4 qv = sq[j * n16 + c + w];
+                            acc[j] += __popc(rv.x & qv.x) + __popc(rv.y & qv.y) + __popc(rv.z & qv.z) +
+                                      __popc(rv.w & qv.w);
+                        }
+                }
+            }
+            __syncwarp();
+        }
+        const uint32_t rl = (uint32_t)r;
+#pragma unroll
+        for (int j = 0; j < QN; ++j) {
+            if (j >= nq) break;
+            const bool cand = valid && acc[j] <= gb[j] && before(acc[j], rl, ks[j], kx[j]);
+            uint32_t m = __ballot_sync(0xFFFFFFFFu, cand);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t v = __shfl_sync(0xFFFFFFFFu, acc[j], src);
+                const uint32_t x = __shfl_sync(0xFFFFFFFFu, rl, src);
+                if (!before(v, x, ks[j], kx[j])) continue;  // an earlier insertion raised the bar
+                // entries before (v, x) stay; the rest shift one lane down
+                const int pos = __popc(__ballot_sync(0xFFFFFFFFu, lane < KP && before(ls[j], lx[j], v, x)));
+                const uint32_t us = __shfl_up_sync(0xFFFFFFFFu, ls[j], 1);
+                const uint32_t ux = __shfl_up_sync(0xFFFFFFFFu, lx[j], 1);
+                if (lane == pos) {
+                    ls[j] = v;
+                    lx[j] = x;
+                } else if (lane > pos && lane < KP) {
+                    ls[j] = us;
+                    lx[j] = ux;
+                }
+                ks[j] = __shfl_sync(0xFFFFFFFFu, ls[j], KP - 1);
+                kx[j] = __shfl_sync(0xFFFFFFFFu, lx[j], KP - 1);
+                if (ks[j] != kEmptyScore) {
+                    if (ks[j] < gb[j]) gb[j] = ks[j];
+                    if (lane == 0) atomicMin(a.bound + j, ks[j]);
+                }
+            }
+        }
+    }
+    // the CTA's warps' lists -> one partial list per unknown (a k-way merge by one warp)
+    __syncthreads();  // every warp is done with the unknowns and staging: the space is reused below
+    uint32_t* ms = reinterpret_cast<uint32_t*>(sq);  // [warps][kScanMaxQ][KP] scores, then indices
+    uint32_t* mx = ms + kScanWarps * kScanMaxQ * KP;
+#pragma unroll
+    for (int j = 0; j < QN; ++j)
+        if (j < nq && lane < KP) {
+            ms[(warp * kScanMaxQ + j) * KP + lane] = ls[j];
+            mx[(warp * kScanMaxQ + j) * KP + lane] = lx[j];
+        }
+    __syncthreads();
+    for (int j = warp; j < nq; j += kScanWarps) {
+        int head = 0;  // lane w < kScanWarps walks warp w's list
+        const int64_t off = ((int64_t)blockIdx.x * a.n_queries + j) * KP;
+        for (int o = 0; o < KP; ++o) {
+            uint32_t hs = kEmptyScore, hx = kEmptyLocal;
+            if (lane < kScanWarps && head < KP) {
+                hs = ms[(lane * kScanMaxQ + j) * KP + head];
+                hx = mx[(lane * kScanMaxQ + j) * KP + head];
+            }
+            uint32_t bs = hs, bx = hx;
+            int bl = lane;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                const uint32_t os = __shfl_xor_sync(0xFFFFFFFFu, bs, d);
+                const uint32_t ox = __shfl_xor_sync(0xFFFFFFFFu, bx, d);
+                const int ol = __shfl_xor_sync(0xFFFFFFFFu, bl, d);
+                if (before(os, ox, bs, bx) || (os == bs && ox == bx && ol < bl)) {
+                    bs = os;
+                    bx = ox;
+                    bl = ol;
+                }
+            }
+            if (lane == bl && bs != kEmptyScore) ++head;
+            if (lane == 0) {
+                a.part_scores[off + o] = bs;
+                a.part_index[off + o] = bs == kEmptyScore ? -1 : a.ref_base + (int64_t)bx;
+            }
+        }
+    }
+}
+
+inline size_t scan_smem_bytes(const CompareArgs& a, int kpad) {
+    const size_t lists = 2 * (size_t)kScanWarps * kScanMaxQ * kpad * 4;
+    const size_t rows = (size_t)a.n_queries * (a.stride / 16) * 16 + (size_t)kScanWarps * kScanTile16 * 16;
+    return rows > lists ? rows : lists;
+}
+
+template <int KP, int QN>
+int launch_scan_q(const CompareArgs& a, int n_ctas, cudaStream_t stream) {
+    const size_t smem = scan_smem_bytes(a, KP);
+    auto kern = popc_scan_kernel<KP, QN>;
+    FASTID_CUDA(ensure_dynamic_smem((const void*)kern, (int)smem));
+    kern<<<(unsigned)n_ctas, 32 * kScanWarps, smem, stream>>>(a);
+    FASTID_LAUNCHED("popc_scan_kernel");
+    return FASTID_OK;
+}
+
+// per-unknown state lives in registers: instantiate for the batch size so a
+// single profile keeps the occupancy of a small kernel
+template <int KP>
+int launch_scan(const CompareArgs& a, int n_ctas, cudaStream_t stream) {
+    if (a.n_queries <= 1) return launch_scan_q<KP, 1>(a, n_ctas, stream);
+    if (a.n_queries <= 2) return launch_scan_q<KP, 2>(a, n_ctas, stream);
+    if (a.n_queries <= 4) return launch_scan_q<KP, 4>(a, n_ctas, stream);
+    if (a.n_queries <= 8) return launch_scan_q<KP, 8>(a, n_ctas, stream);
+    return launch_scan_q<KP, kScanMaxQ>(a, n_ctas, stream);
+}
+
 template <int MODE, int KP>
 int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     const int64_t n_ref_tiles = ceil_div(a.n_refs, kRows);
@@ -214,6 +410,14 @@ int launch_popc(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t stre
     if (mode == kThreshold) return launch_mode<kThreshold, 1>(a, 1, stream);
     const int parts = popc_parts(a.n_refs, a.n_queries);
     *n_parts = parts;
+    // few unknowns (and their rows, plus the merge lists, in shared memory): the scan
+    if (a.n_queries <= kScanMaxQ && scan_smem_bytes(a, a.kpad) <= 200 * 1024) {
+        switch (a.kpad) {
+            case 8: return launch_scan<8>(a, parts, stream);
+            case 16: return launch_scan<16>(a, parts, stream);
+            case 32: return launch_scan<32>(a, parts, stream);
+        }
+    }
     switch (a.kpad) {
         case 8: return launch_mode<kTopK, 8>(a, parts / 2, stream);
         case 16: return launch_mode<kTopK, 16>(a, parts / 2, stream);

@@ -193,6 +193,10 @@ class ChunkedImage:
 # saves: 20M x 16384 loci, top-16 (tools/chunked_vs_packed.py): 64 unknowns 72 ms
 # chunked vs 20 ms packed, 512: 101 vs 75, 1024: 139 vs 152, 2048: 226 vs 306.
 CHUNKED_IMAGE_MIN_QUERIES = 1024
+# Up to this many unknowns an "auto" top-k runs the CUDA-core scan over the packed
+# rows instead of the tensor image (tools/small_batch.py, 20M x 1024 loci, top-16:
+# 1 unknown 0.70 vs 1.52 ms, 2: 1.04 vs 1.52, 4: 1.41 vs 1.54, 8: 2.41 vs 1.55).
+SCAN_MAX_QUERIES = 4
 
 
 class _ChunkView:
@@ -300,6 +304,7 @@ class KnownDatabase:
         # mxf4) keeps only its packed rows and runs the unpacking kernels instead
         self.image = None
         self.chunked_min_queries = CHUNKED_IMAGE_MIN_QUERIES
+        self.scan_max_queries = SCAN_MAX_QUERIES
         if prepare and self.panel.n_profiles:
             # image_chunk_rows: build the image chunk by chunk into one buffer of that
             # many rows (what a panel whose whole image does not fit falls back to)
@@ -357,6 +362,11 @@ class KnownDatabase:
 
     def topk_device(self, queries: DevicePanel, k: int, max_score: int | None = None, workspace=None, out=None,
                     events=None):
+        if (self.formulation == "auto" and queries.n_profiles <= self.scan_max_queries
+                and self.panel.n_profiles and events is None):
+            # a handful of unknowns: the CUDA-core scan over the packed rows (HBM-bound)
+            # beats streaming the 4-bit image (one unknown, 20M x 1024 loci: 0.70 vs 1.52 ms)
+            return topk_device(self.panel, queries, k, max_score, self.ref_base, "popc", workspace, out)
         if self._chunked_for(queries.n_profiles):
             return self._topk_chunked(queries, k, max_score, workspace, out)
         return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out,

@@ -806,3 +806,26 @@ def test_chunked_image_small_batches_use_packed_operands(rng):
     s, x = db.search_words(q, 8)
     es, ex, _ = oracle.topk(r, q, 8, 0xFFFFFFFE)
     assert np.array_equal(s, es) and np.array_equal(x, ex)
+
+
+@pytest.mark.parametrize("n_q", [1, 2, 7, 16])
+@pytest.mark.parametrize("L,width", [(1024, 64), (777, 32), (5000, 64), (64, 64)])
+def test_popc_scan_few_unknowns(rng, n_q, L, width):
+    """The CUDA-core scan for <= 16 unknowns (one packed row per lane, per-warp
+    lists across the lanes, a shared bound, a per-CTA merge): top-k for k = 1, 16,
+    32 with and without a score cap, planted copies and duplicate knowns (ties
+    across warps and CTAs) equal the oracle."""
+    m = fb()
+    n_r = 150_003
+    nw = -(-L // width)
+    r, _ = rand_words(rng, n_r, nw, width, L)
+    q, _ = rand_words(rng, n_q, nw, width, L)
+    q[0] = r[77]
+    r[100_000] = r[77]  # the same known twice: a tie at score 0
+    r[5:9] = r[150_000]
+    R, Q = m.Panel(tuple(range(n_r)), r, L), m.Panel(tuple(range(n_q)), q, L)
+    for k, ms in ((16, None), (1, None), (32, L // 5), (5, 0)):
+        res = m.topk(R, Q, k, max_score=ms, formulation="popc")
+        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE if ms is None else ms)
+        assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), (k, ms)
+    assert 77 in res.index[0] or k < 2
