@@ -197,6 +197,12 @@ CHUNKED_IMAGE_MIN_QUERIES = 1024
 # rows instead of the tensor image (tools/small_batch.py, 20M x 1024 loci, top-16:
 # 1 unknown 0.70 vs 1.52 ms, 2: 1.04 vs 1.52, 4: 1.41 vs 1.54, 8: 2.41 vs 1.55).
 SCAN_MAX_QUERIES = 4
+# Up to this many unknowns (one 128-row group of the single-CTA tensor kernel) an
+# "auto" top-k reads the packed rows, unpacked in shared memory, instead of the
+# 4-bit image: 20M x 1024 loci 8-128 unknowns 1.23-1.35 vs 1.54-1.75 ms; 10M x
+# 2048 loci 1.25-1.36 vs 1.51-1.67; 5M x 5000 1.63-1.79 vs 1.90-2.05; at 256
+# unknowns the image wins (2.16 vs 2.33, 1.92 vs 2.40, 2.14 vs 3.39).
+PACKED_MAX_QUERIES = 128
 
 
 class _ChunkView:
@@ -305,6 +311,7 @@ class KnownDatabase:
         self.image = None
         self.chunked_min_queries = CHUNKED_IMAGE_MIN_QUERIES
         self.scan_max_queries = SCAN_MAX_QUERIES
+        self.packed_max_queries = PACKED_MAX_QUERIES
         if prepare and self.panel.n_profiles:
             # image_chunk_rows: build the image chunk by chunk into one buffer of that
             # many rows (what a panel whose whole image does not fit falls back to)
@@ -362,11 +369,16 @@ class KnownDatabase:
 
     def topk_device(self, queries: DevicePanel, k: int, max_score: int | None = None, workspace=None, out=None,
                     events=None):
-        if (self.formulation == "auto" and queries.n_profiles <= self.scan_max_queries
-                and self.panel.n_profiles and events is None):
-            # a handful of unknowns: the CUDA-core scan over the packed rows (HBM-bound)
-            # beats streaming the 4-bit image (one unknown, 20M x 1024 loci: 0.70 vs 1.52 ms)
-            return topk_device(self.panel, queries, k, max_score, self.ref_base, "popc", workspace, out)
+        if self.formulation == "auto" and self.panel.n_profiles and events is None:
+            n_q = queries.n_profiles
+            if n_q <= self.scan_max_queries:
+                # a handful of unknowns: the CUDA-core scan over the packed rows (HBM-bound)
+                # beats streaming the 4-bit image (one unknown, 20M x 1024 loci: 0.70 vs 1.52 ms)
+                return topk_device(self.panel, queries, k, max_score, self.ref_base, "popc", workspace, out)
+            if n_q <= self.packed_max_queries:
+                # one group of unknowns: the tensor kernel unpacking packed rows in shared
+                # memory reads 4x fewer bytes than the image and is faster
+                return topk_device(self.panel, queries, k, max_score, self.ref_base, "tensor_f4", workspace, out)
         if self._chunked_for(queries.n_profiles):
             return self._topk_chunked(queries, k, max_score, workspace, out)
         return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out,
