@@ -16,7 +16,9 @@ from paper_1707_00516_b200.search import KnownDatabase
 
 n_r, L = (int(x) for x in (sys.argv[1:3] if len(sys.argv) > 2 else (20_000_000, 1024)))
 g = torch.Generator(device="cuda").manual_seed(0)
-r = torch.randint(-(2**63), 2**63 - 1, (n_r, L // 64), dtype=torch.int64, device="cuda", generator=g)
+r = torch.randint(-(2**63), 2**63 - 1, (n_r, -(-L // 64)), dtype=torch.int64, device="cuda", generator=g)
+if L % 64:
+    r[:, -1] &= ~((1 << (64 - L % 64)) - 1)
 panel = m.DevicePanel.from_words(r, L)
 dbs = {f: KnownDatabase(panel, formulation=f) for f in ("tensor_f4", "popc")}
 for n_q in (1, 2, 4, 8, 16, 32, 64, 256):
