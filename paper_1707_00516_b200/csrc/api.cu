@@ -556,7 +556,11 @@ int threshold_impl(const void* refs, const void* image, int options, int64_t n_r
     a.capacity = capacity;
     a.hit_count = hit_count;
     int parts = 0;
-    return launch(kThreshold, a, resolve_formulation(formulation, bit_length), &parts, st);
+    // auto, packed rows, a handful of unknowns: the CUDA-core scan (as for top-k)
+    const int f = (formulation == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
+                      ? FASTID_POPC
+                      : resolve_formulation(formulation, bit_length);
+    return launch(kThreshold, a, f, &parts, st);
 }
 }  // namespace
 

@@ -199,7 +199,7 @@ constexpr int kScanWarps = 8;
 constexpr int kScanPiece = 8;  // uint4 per row per staging round (128 B)
 constexpr int kScanTile16 = 32 * (kScanPiece + 1);  // one warp's staging tile (uint4), padded rows
 
-template <int KP, int QN>
+template <int MODE, int KP, int QN>
 __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_kernel(CompareArgs a) {
     extern __shared__ __align__(16) uint4 sq[];  // [n_queries][n16] complemented unknown rows
     const int n16 = (int)(a.stride / 16);
@@ -270,6 +270,12 @@ __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_ke
             __syncwarp();
         }
         const uint32_t rl = (uint32_t)r;
+        if constexpr (MODE == kThreshold) {
+            // every (unknown, row) within the threshold, appended with warp-aggregated slots
+#pragma unroll
+            for (int j = 0; j < QN; ++j)
+                if (j < nq) emit_hits(a, valid && acc[j] <= a.threshold, (uint32_t)j, r, acc[j]);
+        } else {
 #pragma unroll
         for (int j = 0; j < QN; ++j) {
             if (j >= nq) break;
@@ -300,7 +306,9 @@ __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_ke
                 }
             }
         }
+        }  // top-k
     }
+    if constexpr (MODE == kThreshold) return;
     // the CTA's warps' lists -> one partial list per unknown (a k-way merge by one warp)
     __syncthreads();  // every warp is done with the unknowns and staging: the space is reused below
     uint32_t* ms = reinterpret_cast<uint32_t*>(sq);  // [warps][kScanMaxQ][KP] scores, then indices
@@ -349,10 +357,10 @@ inline size_t scan_smem_bytes(const CompareArgs& a, int kpad) {
     return rows > lists ? rows : lists;
 }
 
-template <int KP, int QN>
+template <int MODE, int KP, int QN>
 int launch_scan_q(const CompareArgs& a, int n_ctas, cudaStream_t stream) {
     const size_t smem = scan_smem_bytes(a, KP);
-    auto kern = popc_scan_kernel<KP, QN>;
+    auto kern = popc_scan_kernel<MODE, KP, QN>;
     FASTID_CUDA(ensure_dynamic_smem((const void*)kern, (int)smem));
     kern<<<(unsigned)n_ctas, 32 * kScanWarps, smem, stream>>>(a);
     FASTID_LAUNCHED("popc_scan_kernel");
@@ -361,13 +369,13 @@ int launch_scan_q(const CompareArgs& a, int n_ctas, cudaStream_t stream) {
 
 // per-unknown state lives in registers: instantiate for the batch size so a
 // single profile keeps the occupancy of a small kernel
-template <int KP>
+template <int MODE, int KP>
 int launch_scan(const CompareArgs& a, int n_ctas, cudaStream_t stream) {
-    if (a.n_queries <= 1) return launch_scan_q<KP, 1>(a, n_ctas, stream);
-    if (a.n_queries <= 2) return launch_scan_q<KP, 2>(a, n_ctas, stream);
-    if (a.n_queries <= 4) return launch_scan_q<KP, 4>(a, n_ctas, stream);
-    if (a.n_queries <= 8) return launch_scan_q<KP, 8>(a, n_ctas, stream);
-    return launch_scan_q<KP, kScanMaxQ>(a, n_ctas, stream);
+    if (a.n_queries <= 1) return launch_scan_q<MODE, KP, 1>(a, n_ctas, stream);
+    if (a.n_queries <= 2) return launch_scan_q<MODE, KP, 2>(a, n_ctas, stream);
+    if (a.n_queries <= 4) return launch_scan_q<MODE, KP, 4>(a, n_ctas, stream);
+    if (a.n_queries <= 8) return launch_scan_q<MODE, KP, 8>(a, n_ctas, stream);
+    return launch_scan_q<MODE, KP, kScanMaxQ>(a, n_ctas, stream);
 }
 
 template <int MODE, int KP>
@@ -407,15 +415,19 @@ int popc_parts(int64_t n_refs, int64_t n_queries) {
 
 int launch_popc(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t stream) {
     if (mode == kFull) return launch_mode<kFull, 1>(a, 1, stream);
-    if (mode == kThreshold) return launch_mode<kThreshold, 1>(a, 1, stream);
+    if (mode == kThreshold) {
+        if (a.n_queries <= kScanMaxQ && scan_smem_bytes(a, 8) <= 200 * 1024)
+            return launch_scan<kThreshold, 8>(a, 4 * num_sms(), stream);
+        return launch_mode<kThreshold, 1>(a, 1, stream);
+    }
     const int parts = popc_parts(a.n_refs, a.n_queries);
     *n_parts = parts;
     // few unknowns (and their rows, plus the merge lists, in shared memory): the scan
     if (a.n_queries <= kScanMaxQ && scan_smem_bytes(a, a.kpad) <= 200 * 1024) {
         switch (a.kpad) {
-            case 8: return launch_scan<8>(a, parts, stream);
-            case 16: return launch_scan<16>(a, parts, stream);
-            case 32: return launch_scan<32>(a, parts, stream);
+            case 8: return launch_scan<kTopK, 8>(a, parts, stream);
+            case 16: return launch_scan<kTopK, 16>(a, parts, stream);
+            case 32: return launch_scan<kTopK, 32>(a, parts, stream);
         }
     }
     switch (a.kpad) {

@@ -534,6 +534,10 @@ class KnownDatabase:
 
     def threshold(self, queries, threshold: int, capacity: int | None = None) -> ThresholdHits:
         n_q = queries.n_profiles if isinstance(queries, DevicePanel) else len(queries.words)
+        if self.formulation == "auto" and n_q <= self.scan_max_queries and self.panel.n_profiles:
+            # a handful of unknowns: the CUDA-core scan over the packed rows
+            return threshold_hits(self.panel, queries, threshold, capacity, "popc", self.device,
+                                  ref_base=self.ref_base)
         if self._chunked_for(n_q):
             parts = [threshold_hits(sub, queries, threshold, capacity, self.formulation, self.device,
                                     ref_base=self.ref_base + r0, image=view)

@@ -829,3 +829,25 @@ def test_popc_scan_few_unknowns(rng, n_q, L, width):
         es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE if ms is None else ms)
         assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), (k, ms)
     assert 77 in res.index[0] or k < 2
+
+
+@pytest.mark.parametrize("n_q", [1, 3, 16])
+@pytest.mark.parametrize("L", [1024, 5000, 130])
+def test_popc_scan_threshold(rng, n_q, L):
+    """Threshold hits of <= 16 unknowns through the CUDA-core scan (one packed row
+    per lane, warp-aggregated hit slots): the (unknown, known, score) list equals
+    the oracle's, with planted copies, duplicate knowns and a capacity overflow
+    that the two-pass wrapper recovers from."""
+    m = fb()
+    n_r = 120_001
+    nw = -(-L // 64)
+    r, _ = rand_words(rng, n_r, nw, 64, L)
+    q, _ = rand_words(rng, n_q, nw, 64, L)
+    q[0] = r[9]
+    r[60_000] = r[9]
+    R, Q = m.Panel(tuple(range(n_r)), r, L), m.Panel(tuple(range(n_q)), q, L)
+    exp = oracle.naive(r, q) if n_r * n_q * L <= 3e9 else oracle.blocked(r, np.ascontiguousarray(q.T), 64, 16, os.cpu_count() or 1)
+    t = int(np.percentile(exp, 0.5))
+    hits = m.threshold_hits(R, Q, t, capacity=7, formulation="popc")
+    hq, hr, hs = oracle.threshold_from_matrix(exp, t)
+    assert np.array_equal(hits.query, hq) and np.array_equal(hits.ref, hr) and np.array_equal(hits.score, hs)
