@@ -92,6 +92,17 @@ def main():
     s, x = g.run(queries.words)
     assert np.array_equal(s, es) and np.array_equal(x, ex), "graphed topk"
     n_cases += 3
+    # the CUDA-core scan (<= 16 unknowns): top-k and threshold
+    refs, queries = panel(rng, 5000, 777, "r"), panel(rng, 3, 777, "q")
+    expected = oracle.naive(refs.words, queries.words)
+    res = fb.topk(refs, queries, 8, formulation="popc")
+    es, ex, _ = oracle.topk_from_matrix(expected, 8)
+    assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), "scan topk"
+    thr = int(np.percentile(expected, 1))
+    hits = fb.threshold_hits(refs, queries, thr, formulation="popc")
+    jj, ii = np.nonzero(expected.T <= thr)
+    assert np.array_equal(hits.query, jj) and np.array_equal(hits.ref, ii), "scan threshold"
+    n_cases += 2
     torch.cuda.synchronize()
     print(f"sanitize cases ok ({n_cases})")
 
