@@ -147,7 +147,8 @@ struct CompareArgs {
     uint32_t* part_scores;  // [n_parts][n_queries][kpad]
     int64_t* part_index;
     int kpad;
-    uint32_t* bound;        // [n_queries] shared top-k admission bound (formulation's raw score bits: admit v < bound), or null
+    uint32_t* bound;        // [n_queries] shared top-k admission bound, 0xFFFFFFFF-initialised per launch: tensor
+                            // kernels keep raw score bits (admit v < bound), the CUDA-core scan a score (admit v <= bound)
     uint32_t* list_min;     // [n_queries][kMinSlots] best value published by each of the first kMinSlots lists
     // CTA-pair kernel: per (slice, unknown group) tile progress, for drift control
     int* progress;

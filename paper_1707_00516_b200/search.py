@@ -19,7 +19,8 @@ import ctypes
 import numpy as np
 import torch
 
-from .compare import DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device
+from .compare import (DevicePanel, _check_panels, _require_cuda, compare_device, threshold_hits, topk_device,
+                      topk_workspace_bytes)
 from .panel import ThresholdHits, TopKResult
 
 __all__ = ["KnownDatabase", "PreparedImage", "ChunkedImage", "QueryStager", "GraphedSearch", "DB_OPTIONS"]
@@ -235,9 +236,8 @@ class GraphedSearch:
         self.stager = QueryStager(self.n_queries, p.n_words, p.word_width, p.bit_length, self.k, dev)
         st = self.stager
         with torch.cuda.device(dev):
-            st.workspace = torch.empty(
-                topk_workspace_bytes_for(p.n_profiles, self.n_queries, self.k, db.formulation), dtype=torch.uint8,
-                device=dev)
+            st.workspace = torch.empty(topk_workspace_bytes(p.n_profiles, self.n_queries, self.k, db.formulation),
+                                       dtype=torch.uint8, device=dev)
             self.stream = torch.cuda.Stream(dev)
             self.stream.wait_stream(torch.cuda.current_stream(dev))
             lib = _native.lib()
@@ -280,12 +280,6 @@ class GraphedSearch:
             self.graph.replay()
         self.stream.synchronize()
         return st.host_s.numpy().view(np.uint32).copy(), st.host_x.numpy().copy()
-
-
-def topk_workspace_bytes_for(n_refs: int, n_queries: int, k: int, formulation) -> int:
-    from .compare import topk_workspace_bytes
-
-    return topk_workspace_bytes(n_refs, n_queries, k, formulation)
 
 
 class KnownDatabase:
