@@ -63,6 +63,21 @@ enum fastid_formulation {
     FASTID_TENSOR_F4 = 3   /* tcgen05.mma kind::mxf4 (e2m1 0/1, unit scales)    */
 };
 
+/* The overloaded semiring's "multiply" (FastID Eq. 1 and the paper's variants,
+ * PAPER.md:39-45), OR-ed into any `formulation` argument:
+ *   FASTID_OP_ANDNOT  popcount(known AND NOT unknown) -- the reference's score
+ *                     (kernel.py:33-35); the default (0)
+ *   FASTID_OP_AND     popcount(known AND unknown): shared minor alleles
+ *   FASTID_OP_XOR     popcount(known XOR unknown): Hamming distance
+ * The reference implements only AND-NOT; AND and XOR have no reference
+ * counterpart and are checked against a numpy restatement. */
+enum fastid_operator {
+    FASTID_OP_ANDNOT = 0,
+    FASTID_OP_AND = 0x100,
+    FASTID_OP_XOR = 0x200
+};
+#define FASTID_OP_MASK 0x300
+
 FASTID_API int fastid_abi_version(void);
 FASTID_API const char* fastid_last_error(void);
 /* bytes per device row for a panel of bit_length loci: ceil(L / 128) * 16 */
@@ -161,6 +176,9 @@ FASTID_API int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride
 FASTID_API int fastid_db_create_in(const void* refs, int64_t n_refs, int64_t stride, int64_t bit_length,
                                    int formulation, void* image, size_t image_bytes, void* stream, fastid_db** out);
 FASTID_API int fastid_db_destroy(fastid_db* db);
+/* The operator (FASTID_OP_*) of the handle's later comparisons (default
+ * AND-NOT).  XOR needs each known row's popcount: computed once on first use. */
+FASTID_API int fastid_db_set_operator(fastid_db* db, int op);
 FASTID_API int fastid_db_formulation(const fastid_db* db);
 
 /* Execution variants of a prepared database.  Every option computes the same

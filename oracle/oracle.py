@@ -197,6 +197,23 @@ def np_scores(refs: np.ndarray, queries: np.ndarray) -> np.ndarray:
     return np.bitwise_count(r & ~q).sum(axis=2, dtype=np.uint32)
 
 
+def np_scores_op(refs: np.ndarray, queries: np.ndarray, op: str = "andnot", block: int = 4096) -> np.ndarray:
+    """sum_k popcount(op(r_k, q_k)) for op in {"andnot", "and", "xor"}.
+
+    "andnot" is Eq. 1 (pinned by the golden fixtures through np_scores and
+    the C oracle).  "and" and "xor" are operator extensions the reference
+    does not implement -- their restatement is the definition itself
+    (popcount of the word-wise AND / XOR), PARITY UNPINNED against the
+    reference.  Blocked over known rows to bound the temporary."""
+    fn = {"andnot": lambda r, q: r & ~q, "and": lambda r, q: r & q, "xor": lambda r, q: r ^ q}[op]
+    out = np.empty((refs.shape[0], queries.shape[0]), dtype=np.uint32)
+    q = queries[None, :, :]
+    for r0 in range(0, refs.shape[0], block):
+        r = refs[r0:r0 + block, None, :]
+        out[r0:r0 + block] = np.bitwise_count(fn(r, q)).sum(axis=2, dtype=np.uint32)
+    return out
+
+
 def topk_from_matrix(scores: np.ndarray, k: int, max_score: int = 0xFFFFFFFF):
     """The same top-k derivation from a full (N_R, N_Q) matrix (numpy, stable)."""
     n_r, n_q = scores.shape

@@ -34,6 +34,10 @@ NVCC_FLAGS = (
 
 FASTID_OK, E_INVALID, E_MISMATCH, E_CUDA, E_CAPACITY, E_NOMEM, E_UNSUPPORTED, E_FORMAT, E_CORRUPT = range(9)
 FORMULATIONS = {"auto": 0, "popc": 1, "tensor_i8": 2, "tensor_f4": 3}
+# The bitwise operator before the popcount (enum fastid_operator, carried in
+# bits 8-9 of a formulation argument): r AND NOT q (FastID Eq. 1, the
+# default), r AND q (shared ones), r XOR q (Hamming distance).
+OPERATORS = {"andnot": 0, "and": 0x100, "xor": 0x200}
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None
@@ -141,6 +145,7 @@ def _signatures() -> dict:
         "fastid_db_destroy": ([vp], i32),
         "fastid_db_formulation": ([vp], i32),
         "fastid_db_set_option": ([vp, i32, i32], i32),
+        "fastid_db_set_operator": ([vp, i32], i32),
         "fastid_db_options": ([vp], i32),
         "fastid_db_compare_full": ([vp, vp, i64, vp, i64, vp], i32),
         "fastid_db_topk_partials": ([vp, vp, i64, i32, u32, i64, vp, sz, vp, ctypes.POINTER(i32),
@@ -227,10 +232,17 @@ def supports(formulation: str | int, bit_length: int) -> bool:
     return bool(lib().fastid_supports(formulation_code(formulation), int(bit_length)))
 
 
-def formulation_code(name: str | int) -> int:
-    if isinstance(name, int):
-        return name
+def operator_code(op: str) -> int:
     try:
-        return FORMULATIONS[name]
+        return OPERATORS[op]
+    except KeyError:
+        raise ValueError(f"op must be one of {sorted(OPERATORS)}, got {op!r}") from None
+
+
+def formulation_code(name: str | int, op: str = "andnot") -> int:
+    if isinstance(name, int):
+        return name | operator_code(op)
+    try:
+        return FORMULATIONS[name] | operator_code(op)
     except KeyError:
         raise ValueError(f"formulation must be one of {sorted(FORMULATIONS)}, got {name!r}") from None

@@ -255,10 +255,21 @@ def _ptr(p: DevicePanel) -> int:
     return p.rows.data_ptr() if p.n_profiles else 0
 
 
+def _check_image_op(image, op: str) -> None:
+    _native.operator_code(op)
+    if image is not None and getattr(image, "op", "andnot") != op:
+        raise ValueError(f"the prepared image was built for op={image.op!r}, not {op!r}")
+
+
 def compare_device(refs: DevicePanel, queries: DevicePanel, out: torch.Tensor | None = None,
-                   formulation: str | int = "auto", image=None) -> torch.Tensor:
-    """Full (N_R, N_Q) u32 score matrix on the device (int32 storage, reinterpret as u32)."""
+                   formulation: str | int = "auto", image=None, op: str = "andnot") -> torch.Tensor:
+    """Full (N_R, N_Q) u32 score matrix on the device (int32 storage, reinterpret as u32).
+
+    ``op`` is the bitwise operator before the popcount: "andnot" (FastID Eq. 1,
+    popcount(r AND NOT q)), "and" (popcount(r AND q)) or "xor" (Hamming distance).
+    """
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    _check_image_op(image, op)
     dev = refs.device
     if out is None:
         out = torch.empty((refs.n_profiles, queries.n_profiles), dtype=torch.int32, device=dev)
@@ -275,7 +286,7 @@ def compare_device(refs: DevicePanel, queries: DevicePanel, out: torch.Tensor | 
             else:
                 _native.check(_native.lib().fastid_compare_full(
                     _ptr(refs), refs.n_profiles, _ptr(queries), queries.n_profiles, refs.stride,
-                    refs.bit_length, out.data_ptr(), out.stride(0), _native.formulation_code(formulation),
+                    refs.bit_length, out.data_ptr(), out.stride(0), _native.formulation_code(formulation, op),
                     _stream(dev)), "fastid_compare_full")
     return out
 
@@ -290,9 +301,11 @@ def _score_matrix_type(panel):
     return cls if isinstance(cls, type) else ScoreMatrix
 
 
-def compare_b200(refs, queries, formulation: str | int = "auto", device=None):
+def compare_b200(refs, queries, formulation: str | int = "auto", device=None, op: str = "andnot"):
     """``compare_naive`` on the B200 (kernel.py:283-292): same signature, errors,
-    empties and result type (the reference's ScoreMatrix for reference panels)."""
+    empties and result type (the reference's ScoreMatrix for reference panels).
+    ``op`` as in compare_device (the reference computes "andnot" only)."""
+    _native.operator_code(op)
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
     result = _score_matrix_type(refs)
     n_r, n_q = refs.words.shape[0], queries.words.shape[0]
@@ -307,9 +320,9 @@ def compare_b200(refs, queries, formulation: str | int = "auto", device=None):
         # host-buffer ABI instead of one device-sized matrix and a pageable copy
         scores = np.empty((n_r, n_q), np.uint32)
         with torch.cuda.device(dev):
-            run_b200_kernel(refs.words, queries.words, scores, formulation=formulation)
+            run_b200_kernel(refs.words, queries.words, scores, formulation=formulation, op=op)
         return result(ref_ids, q_ids, scores)
-    d = compare_device(_as_device(refs, dev), _as_device(queries, dev), formulation=formulation)
+    d = compare_device(_as_device(refs, dev), _as_device(queries, dev), formulation=formulation, op=op)
     scores = d.cpu().numpy().view(np.uint32)
     return result(ref_ids, q_ids, scores)
 
@@ -341,7 +354,7 @@ def compare_blocked_b200(refs, queries: QueryLayout, tile: TileConfig | None = N
 
 
 def run_b200_kernel(ref_words: np.ndarray, query_words: np.ndarray, out: np.ndarray,
-                    queries_transposed: bool = False, formulation: str | int = "auto") -> None:
+                    queries_transposed: bool = False, formulation: str | int = "auto", op: str = "andnot") -> None:
     """Raw-array dispatch through the C ABI's host-buffer entry (fastid_run_kernel).
 
     Matches run_naive_kernel (kernel.py:350-353) -- and run_blocked_kernel
@@ -364,7 +377,7 @@ def run_b200_kernel(ref_words: np.ndarray, query_words: np.ndarray, out: np.ndar
     _require_cuda()
     _native.check(_native.lib().fastid_run_kernel(
         ref_words.ctypes.data, n_refs, query_words.ctypes.data, n_q, n_words, ref_words.dtype.itemsize * 8,
-        int(bool(queries_transposed)), out.ctypes.data, _native.formulation_code(formulation)),
+        int(bool(queries_transposed)), out.ctypes.data, _native.formulation_code(formulation, op)),
         "fastid_run_kernel")
 
 
@@ -429,15 +442,18 @@ def topk_workspace_bytes(n_refs: int, n_queries: int, k: int, formulation: str |
 
 def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int | None = None,
                 ref_base: int = 0, formulation: str | int = "auto", workspace: torch.Tensor | None = None,
-                out: tuple | None = None, events: tuple | None = None, image=None):
+                out: tuple | None = None, events: tuple | None = None, image=None, op: str = "andnot"):
     """Fused compare + top-k on the device -> (scores int32 [N_Q, k] as u32, index int64 [N_Q, k]).
 
     On the current stream: the comparison kernel (writing per-CTA candidate
     lists; with a prepared mxf4 image also the spare-pair grid, forked to a
     side stream and joined back) and the merge kernel.  ``events=(start, end)``
-    are recorded around the comparison alone (roofline timing).
+    are recorded around the comparison alone (roofline timing).  Every ``op``
+    ranks by (score asc, index asc): nearest by AND-NOT or Hamming distance,
+    fewest shared ones for "and".
     """
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    _check_image_op(image, op)
     L = _native.lib()
     max_k = L.fastid_max_k()
     if not 1 <= k <= max_k:
@@ -472,7 +488,7 @@ def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int 
         else:
             _native.check(L.fastid_topk_partials(
                 _ptr(refs), refs.n_profiles, _ptr(queries), n_q, refs.stride, refs.bit_length, k, ms, ref_base,
-                workspace.data_ptr(), workspace.numel(), _native.formulation_code(formulation), stream.cuda_stream,
+                workspace.data_ptr(), workspace.numel(), _native.formulation_code(formulation, op), stream.cuda_stream,
                 ctypes.byref(lists), ctypes.byref(kp), ctypes.byref(xo), ctypes.byref(so)), "fastid_topk_partials")
         if events is not None:
             events[1].record(stream)
@@ -483,19 +499,19 @@ def topk_device(refs: DevicePanel, queries: DevicePanel, k: int, max_score: int 
 
 
 def topk(refs, queries, k: int, max_score: int | None = None, formulation: str | int = "auto",
-         device=None) -> TopKResult:
+         device=None, op: str = "andnot") -> TopKResult:
     """Per unknown, the k closest knowns by (score asc, known index asc), optionally score <= max_score."""
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
     dev = _require_cuda(device)
     dr, dq = _as_device(refs, dev), _as_device(queries, dev)
-    s, x = topk_device(dr, dq, k, max_score, 0, formulation)
+    s, x = topk_device(dr, dq, k, max_score, 0, formulation, op=op)
     q_ids = getattr(queries, "ids", None) or tuple(f"q{j}" for j in range(dq.n_profiles))
     return TopKResult(tuple(q_ids), s.cpu().numpy().view(np.uint32), x.cpu().numpy(),
                       getattr(refs, "ids", None))
 
 
 def topk_streamed(refs, queries, k: int, max_score: int | None = None, formulation: str | int = "auto",
-                  chunk_rows: int = 0, ref_base: int = 0) -> TopKResult:
+                  chunk_rows: int = 0, ref_base: int = 0, op: str = "andnot") -> TopKResult:
     """``topk`` for a known panel kept in HOST memory, larger than the device if need be.
 
     The panel's rows stream through the GPU in chunks (fastid_run_topk: pinned
@@ -527,14 +543,16 @@ def topk_streamed(refs, queries, k: int, max_score: int | None = None, formulati
         _native.check(L.fastid_run_topk(
             rw.ctypes.data if n_r else None, n_r, qw.ctypes.data, n_q, rw.shape[1], rw.dtype.itemsize * 8, k, ms,
             int(ref_base), scores.ctypes.data, index.ctypes.data, int(chunk_rows),
-            _native.formulation_code(formulation)), "fastid_run_topk")
+            _native.formulation_code(formulation, op)), "fastid_run_topk")
     return TopKResult(tuple(q_ids), scores, index, getattr(refs, "ids", None))
 
 
 def threshold_hits(refs, queries, threshold: int, capacity: int | None = None,
-                   formulation: str | int = "auto", device=None, ref_base: int = 0, image=None) -> ThresholdHits:
+                   formulation: str | int = "auto", device=None, ref_base: int = 0, image=None,
+                   op: str = "andnot") -> ThresholdHits:
     """Every (unknown j, known i, score) with score <= threshold, ordered by (j, i)."""
     _check_panels(refs.bit_length, refs.word_width, queries.bit_length, queries.word_width)
+    _check_image_op(image, op)
     dev = _require_cuda(device)
     dr, dq = _as_device(refs, dev), _as_device(queries, dev)
     cap = int(capacity) if capacity is not None else max(1 << 16, 4 * dq.n_profiles)
@@ -552,7 +570,7 @@ def threshold_hits(refs, queries, threshold: int, capacity: int | None = None,
                 _native.check(_native.lib().fastid_compare_threshold(
                     _ptr(dr), dr.n_profiles, _ptr(dq), dq.n_profiles, dr.stride, dr.bit_length, int(threshold),
                     ref_base, hq.data_ptr(), hr.data_ptr(), hs.data_ptr(), cap, count.data_ptr(),
-                    _native.formulation_code(formulation), _stream(dev)), "fastid_compare_threshold")
+                    _native.formulation_code(formulation, op), _stream(dev)), "fastid_compare_threshold")
         n = int(count.item())
         if n <= cap:
             break

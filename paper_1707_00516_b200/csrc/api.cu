@@ -71,6 +71,7 @@ namespace {
 int list_size_for(int k) { return k <= 8 ? 8 : (k <= 16 ? 16 : 32); }
 
 int resolve_formulation(int formulation, int64_t bit_length) {
+    formulation &= ~FASTID_OP_MASK;
     if (formulation == FASTID_AUTO) {
         return tensor_supported(bit_length, FASTID_TENSOR_F4) ? FASTID_TENSOR_F4 : FASTID_POPC;
     }
@@ -86,6 +87,10 @@ int check_compare(const void* refs, int64_t n_refs, const void* queries, int64_t
                     (long long)bit_length);
     if ((n_refs && ((uintptr_t)refs & 15)) || (n_queries && ((uintptr_t)queries & 15)))
         FASTID_FAIL(FASTID_E_INVALID, "panel rows must be 16-byte aligned");
+    const int op = formulation & FASTID_OP_MASK;
+    if (op != FASTID_OP_ANDNOT && op != FASTID_OP_AND && op != FASTID_OP_XOR)
+        FASTID_FAIL(FASTID_E_INVALID, "unknown operator 0x%x", op);
+    formulation &= ~FASTID_OP_MASK;
     if (formulation < FASTID_AUTO || formulation > FASTID_TENSOR_F4)
         FASTID_FAIL(FASTID_E_INVALID, "unknown formulation %d", formulation);
     if (formulation >= FASTID_TENSOR_I8 && !tensor_supported(bit_length, formulation))
@@ -411,6 +416,9 @@ extern "C" int64_t fastid_row_stride(int64_t bit_length) { return bit_length > 0
 extern "C" int fastid_max_k(void) { return kMaxTopK; }
 extern "C" int fastid_supports(int formulation, int64_t bit_length) {
     if (bit_length <= 0) return 0;
+    const int op = formulation & FASTID_OP_MASK;
+    if (op != FASTID_OP_ANDNOT && op != FASTID_OP_AND && op != FASTID_OP_XOR) return 0;
+    formulation &= ~FASTID_OP_MASK;
     if (formulation == FASTID_AUTO || formulation == FASTID_POPC) return 1;
     return tensor_supported(bit_length, formulation) ? 1 : 0;
 }
@@ -418,13 +426,15 @@ extern "C" int fastid_supports(int formulation, int64_t bit_length) {
 namespace {
 int compare_full_impl(const void* refs, const void* image, int options, int64_t n_refs, const void* queries, int64_t n_queries,
                       int64_t stride, int64_t bit_length, uint32_t* out, int64_t ld_out, int formulation,
-                      void* stream) {
+                      void* stream, const uint32_t* ref_popc = nullptr) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (ld_out < n_queries) FASTID_FAIL(FASTID_E_INVALID, "ld_out smaller than n_queries");
     if (n_refs == 0 || n_queries == 0) return FASTID_OK;
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
     a.image = (const uint8_t*)image;
     a.options = options;
+    a.op = formulation & FASTID_OP_MASK;
+    a.ref_popc = ref_popc;
     a.out = out;
     a.ld_out = ld_out;
     int parts = 0;
@@ -461,7 +471,7 @@ namespace {
 int topk_partials_impl(const void* refs, const void* image, int options, int64_t n_refs, const void* queries, int64_t n_queries,
                        int64_t stride, int64_t bit_length, int k, uint32_t max_score, int64_t ref_base,
                        void* workspace, size_t workspace_bytes, int formulation, void* stream, int* n_lists,
-                       int* list_len, size_t* index_offset, size_t* score_offset) {
+                       int* list_len, size_t* index_offset, size_t* score_offset, const uint32_t* ref_popc = nullptr) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (k < 1 || k > kMaxTopK) FASTID_FAIL(FASTID_E_INVALID, "k must be in [1, %d]", kMaxTopK);
     if (!n_lists || !list_len || !index_offset || !score_offset) FASTID_FAIL(FASTID_E_INVALID, "NULL out-param");
@@ -474,7 +484,7 @@ int topk_partials_impl(const void* refs, const void* image, int options, int64_t
     // auto, packed rows, a handful of unknowns: the CUDA-core scan reads the packed
     // rows once and beats the tensor kernels there (20M x 1024 loci, top-16:
     // 1 unknown 0.70 vs 1.52 ms, 4: 1.41 vs 1.54, 8: 2.41 vs 1.55; popc.cu)
-    const int f = (formulation == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
+    const int f = ((formulation & ~FASTID_OP_MASK) == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
                       ? FASTID_POPC
                       : resolve_formulation(formulation, bit_length);
     const int kp = list_size_for(k);
@@ -482,6 +492,8 @@ int topk_partials_impl(const void* refs, const void* image, int options, int64_t
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
     a.image = (const uint8_t*)image;
     a.options = options;
+    a.op = formulation & FASTID_OP_MASK;
+    a.ref_popc = ref_popc;
     a.k = k;
     a.kpad = kp;
     a.max_score = max_score;
@@ -539,7 +551,7 @@ namespace {
 int threshold_impl(const void* refs, const void* image, int options, int64_t n_refs, const void* queries, int64_t n_queries,
                    int64_t stride, int64_t bit_length, uint32_t threshold, int64_t ref_base, uint32_t* hit_query,
                    int64_t* hit_ref, uint32_t* hit_score, int64_t capacity, unsigned long long* hit_count,
-                   int formulation, void* stream) {
+                   int formulation, void* stream, const uint32_t* ref_popc = nullptr) {
     if (int rc = check_compare(refs, n_refs, queries, n_queries, stride, bit_length, formulation)) return rc;
     if (capacity < 0 || !hit_count) FASTID_FAIL(FASTID_E_INVALID, "bad hit buffers");
     cudaStream_t st = (cudaStream_t)stream;
@@ -548,6 +560,8 @@ int threshold_impl(const void* refs, const void* image, int options, int64_t n_r
     CompareArgs a = make_args(refs, n_refs, queries, n_queries, stride, bit_length);
     a.image = (const uint8_t*)image;
     a.options = options;
+    a.op = formulation & FASTID_OP_MASK;
+    a.ref_popc = ref_popc;
     a.threshold = threshold;
     a.ref_base = ref_base;
     a.hit_query = hit_query;
@@ -557,7 +571,7 @@ int threshold_impl(const void* refs, const void* image, int options, int64_t n_r
     a.hit_count = hit_count;
     int parts = 0;
     // auto, packed rows, a handful of unknowns: the CUDA-core scan (as for top-k)
-    const int f = (formulation == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
+    const int f = ((formulation & ~FASTID_OP_MASK) == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
                       ? FASTID_POPC
                       : resolve_formulation(formulation, bit_length);
     return launch(kThreshold, a, f, &parts, st);
@@ -584,6 +598,8 @@ struct fastid_db {
     int device;
     int options;      // FASTID_OPT_* bits
     bool owns_image;  // false: the caller's buffer (fastid_db_create_in)
+    int op = FASTID_OP_ANDNOT;        // fastid_db_set_operator
+    uint32_t* ref_popc = nullptr;     // per-row popcounts (XOR on the tensor image), owned
 };
 
 extern "C" size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation) {
@@ -599,6 +615,7 @@ extern "C" int fastid_db_create(const void* refs, int64_t n_refs, int64_t stride
     if (int rc = check_compare(refs, n_refs, refs, 0, stride, bit_length, formulation)) return rc;
     auto* db = new fastid_db{refs, n_refs, stride, bit_length, resolve_formulation(formulation, bit_length),
                              nullptr, 0, 0, 0, true};
+    db->op = formulation & FASTID_OP_MASK;
     cudaGetDevice(&db->device);
     if (db->formulation != FASTID_POPC && n_refs > 0) {
         db->image_bytes = tensor_image_bytes(n_refs, bit_length, db->formulation);
@@ -629,6 +646,7 @@ extern "C" int fastid_db_create_in(const void* refs, int64_t n_refs, int64_t str
     if (need && (!image || image_bytes < need))
         FASTID_FAIL(FASTID_E_CAPACITY, "image buffer of %zu bytes is smaller than the %zu required", image_bytes, need);
     auto* db = new fastid_db{refs, n_refs, stride, bit_length, f, need ? image : nullptr, need, 0, 0, false};
+    db->op = formulation & FASTID_OP_MASK;
     cudaGetDevice(&db->device);
     if (need) {
         CompareArgs a = make_args(refs, n_refs, refs, 0, stride, bit_length);
@@ -641,8 +659,43 @@ extern "C" int fastid_db_create_in(const void* refs, int64_t n_refs, int64_t str
     return FASTID_OK;
 }
 
+extern "C" int fastid_db_set_operator(fastid_db* db, int op) {
+    if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    if (op != FASTID_OP_ANDNOT && op != FASTID_OP_AND && op != FASTID_OP_XOR)
+        FASTID_FAIL(FASTID_E_INVALID, "unknown operator 0x%x", op);
+    db->op = op;
+    return FASTID_OK;
+}
+
+namespace {
+// XOR on the image: the rows' popcounts, computed once per handle on the first XOR call
+int db_ref_popc(fastid_db* db, void* stream, const uint32_t** out) {
+    *out = nullptr;
+    if (db->op != FASTID_OP_XOR || db->formulation == FASTID_POPC || db->n_refs == 0) return FASTID_OK;
+    if (!db->ref_popc) {
+        if (cudaMalloc(&db->ref_popc, (size_t)db->n_refs * sizeof(uint32_t)) != cudaSuccess) {
+            cudaGetLastError();
+            db->ref_popc = nullptr;
+            FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)db->n_refs);
+        }
+        if (int rc = launch_row_popcount((const uint8_t*)db->refs, db->n_refs, db->stride, db->ref_popc,
+                                         (cudaStream_t)stream))
+            return rc;
+    }
+    *out = db->ref_popc;
+    return FASTID_OK;
+}
+}  // namespace
+
 extern "C" int fastid_db_destroy(fastid_db* db) {
     if (!db) return FASTID_OK;
+    if (db->ref_popc) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(db->device);
+        cudaFree(db->ref_popc);
+        cudaSetDevice(cur);
+    }
     if (db->image && db->owns_image) {
         int cur = 0;
         cudaGetDevice(&cur);
@@ -672,8 +725,10 @@ extern "C" int fastid_db_options(const fastid_db* db) { return db ? db->options 
 extern "C" int fastid_db_compare_full(const fastid_db* db, const void* queries, int64_t n_queries, uint32_t* out,
                                       int64_t ld_out, void* stream) {
     if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    const uint32_t* pr = nullptr;
+    if (int rc = db_ref_popc(const_cast<fastid_db*>(db), stream, &pr)) return rc;
     return compare_full_impl(db->refs, db->image, db->options, db->n_refs, queries, n_queries, db->stride, db->bit_length, out,
-                             ld_out, db->formulation, stream);
+                             ld_out, db->formulation | db->op, stream, pr);
 }
 
 extern "C" int fastid_db_topk_partials(const fastid_db* db, const void* queries, int64_t n_queries, int k,
@@ -681,9 +736,11 @@ extern "C" int fastid_db_topk_partials(const fastid_db* db, const void* queries,
                                        void* stream, int* n_lists, int* list_len, size_t* index_offset,
                                        size_t* score_offset) {
     if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    const uint32_t* pr = nullptr;
+    if (int rc = db_ref_popc(const_cast<fastid_db*>(db), stream, &pr)) return rc;
     return topk_partials_impl(db->refs, db->image, db->options, db->n_refs, queries, n_queries, db->stride, db->bit_length, k,
-                              max_score, ref_base, workspace, workspace_bytes, db->formulation, stream, n_lists,
-                              list_len, index_offset, score_offset);
+                              max_score, ref_base, workspace, workspace_bytes, db->formulation | db->op, stream, n_lists,
+                              list_len, index_offset, score_offset, pr);
 }
 
 extern "C" int fastid_db_compare_threshold(const fastid_db* db, const void* queries, int64_t n_queries,
@@ -691,8 +748,10 @@ extern "C" int fastid_db_compare_threshold(const fastid_db* db, const void* quer
                                            int64_t* hit_ref, uint32_t* hit_score, int64_t capacity,
                                            unsigned long long* hit_count, void* stream) {
     if (!db) FASTID_FAIL(FASTID_E_INVALID, "db is NULL");
+    const uint32_t* pr = nullptr;
+    if (int rc = db_ref_popc(const_cast<fastid_db*>(db), stream, &pr)) return rc;
     return threshold_impl(db->refs, db->image, db->options, db->n_refs, queries, n_queries, db->stride, db->bit_length, threshold,
-                          ref_base, hit_query, hit_ref, hit_score, capacity, hit_count, db->formulation, stream);
+                          ref_base, hit_query, hit_ref, hit_score, capacity, hit_count, db->formulation | db->op, stream, pr);
 }
 
 namespace {
@@ -931,7 +990,8 @@ extern "C" int fastid_run_topk(const void* ref_words, int64_t n_refs, const void
         int lists = 0, kp = 0;
         size_t xo = 0, so = 0;
         if (int rc = topk_partials_impl(ctx->tk[0], img_bytes ? ctx->tk[1] : nullptr, 0, nr, ctx->buf[2], n_queries,
-                                        stride, bit_length, k, max_score, ref_base + r0, ctx->tk[2], ws_bytes, f, st,
+                                        stride, bit_length, k, max_score, ref_base + r0, ctx->tk[2], ws_bytes,
+                                        f | (formulation & FASTID_OP_MASK), st,
                                         &lists, &kp, &xo, &so))
             return rc;
         const uint32_t* ps = (const uint32_t*)((uint8_t*)ctx->tk[2] + so);

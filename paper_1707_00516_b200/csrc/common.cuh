@@ -162,6 +162,11 @@ struct CompareArgs {
     // CTA-pair kernel: spare pairs and the tiles the regular slices cover (the rest go to spares)
     int n_spare;
     int64_t t_main;
+    // operator (FASTID_OP_*) and, for XOR on the tensor kernels (which accumulate
+    // popcount(known AND unknown)), the rows' popcounts: xor = pr + pq - 2 * and
+    int op;
+    const uint32_t* ref_popc;    // [n_refs]
+    const uint32_t* query_popc;  // [n_queries]
     // threshold
     uint32_t threshold;
     int64_t ref_base;
@@ -239,6 +244,8 @@ int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation);
 int tensor_supported(int64_t bit_length, int formulation);
 size_t tensor_image_bytes(int64_t n_refs, int64_t bit_length, int formulation);
+// popcount of each of `n` rows of `stride` bytes -> out[n] (u32), on `stream`
+int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, uint32_t* out, cudaStream_t stream);
 int build_tensor_image(const CompareArgs& a, int formulation, void* image, cudaStream_t stream);
 int launch_merge(const uint32_t* cand_scores, const int64_t* cand_index, int n_lists,
                  int64_t n_queries, int k_in, int k, uint32_t* top_scores, int64_t* top_index,

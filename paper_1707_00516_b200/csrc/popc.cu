@@ -31,6 +31,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// The comparison operator on one word pair (FASTID_OP_*): LOP3 either way.
+template <int OP>
+__device__ __forceinline__ uint32_t pop_op(uint32_t r, uint32_t q) {
+    if constexpr (OP == FASTID_OP_AND) return __popc(r & q);
+    else if constexpr (OP == FASTID_OP_XOR) return __popc(r ^ q);
+    else return __popc(r & ~q);
+}
+template <int OP>
+__device__ __forceinline__ uint32_t pop_op4(const uint4& r, const uint4& q) {
+    return pop_op<OP>(r.x, q.x) + pop_op<OP>(r.y, q.y) + pop_op<OP>(r.z, q.z) + pop_op<OP>(r.w, q.w);
+}
+
 // Stage chunk `kc` of the known tile (rows r0..) and unknown tile (rows q0..).
 __device__ __forceinline__ void load_stage(const CompareArgs& a, uint8_t* stage, int64_t r0, int64_t q0, int kc) {
     const int64_t kbyte = (int64_t)kc * kChunkWords * 4;
@@ -52,7 +64,7 @@ __device__ __forceinline__ void load_stage(const CompareArgs& a, uint8_t* stage,
     }
 }
 
-template <int MODE, int KP>
+template <int MODE, int KP, int OP>
 __global__ void __launch_bounds__(kThreads, MODE == kTopK ? 1 : 2) popc_kernel(CompareArgs a, int64_t n_ref_tiles, int n_slices) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int tx = threadIdx.x & 15;
@@ -111,8 +123,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kTopK ? 1 : 2) popc_kernel(C
                     const uint4 qv = sq[kk * kRows + tx + 16 * j];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        acc[i][j] += __popc(rv[i].x & ~qv.x) + __popc(rv[i].y & ~qv.y) +
-                                     __popc(rv[i].z & ~qv.z) + __popc(rv[i].w & ~qv.w);
+                        acc[i][j] += pop_op4<OP>(rv[i], qv);
                     }
                 }
             }
@@ -199,16 +210,16 @@ constexpr int kScanWarps = 8;
 constexpr int kScanPiece = 8;  // uint4 per row per staging round (128 B)
 constexpr int kScanTile16 = 32 * (kScanPiece + 1);  // one warp's staging tile (uint4), padded rows
 
-template <int MODE, int KP, int QN>
+template <int MODE, int KP, int QN, bool XOR>
 __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_kernel(CompareArgs a) {
-    extern __shared__ __align__(16) uint4 sq[];  // [n_queries][n16] complemented unknown rows
+    extern __shared__ __align__(16) uint4 sq[];  // [n_queries][n16] unknown rows (complemented for AND-NOT)
     const int n16 = (int)(a.stride / 16);
     const int nq = (int)a.n_queries;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint4* tile = sq + nq * n16 + warp * kScanTile16;  // this warp's staging tile
     for (int i = threadIdx.x; i < nq * n16; i += blockDim.x) {
         const uint4 v = reinterpret_cast<const uint4*>(a.queries)[(int64_t)(i / n16) * n16 + i % n16];
-        sq[i] = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
+        sq[i] = a.op == FASTID_OP_ANDNOT ? make_uint4(~v.x, ~v.y, ~v.z, ~v.w) : v;
     }
     // zero padding in the known rows makes the complemented padding of the
     // unknowns harmless (r & ~q = 0 past L)
@@ -262,8 +273,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_ke
                     for (int j = 0; j < QN; ++j)
                         if (j < nq) {
                             const uint4 qv = sq[j * n16 + c + w];
-                            acc[j] += __popc(rv.x & qv.x) + __popc(rv.y & qv.y) + __popc(rv.z & qv.z) +
-                                      __popc(rv.w & qv.w);
+                            acc[j] += XOR ? pop_op4<FASTID_OP_XOR>(rv, qv) : pop_op4<FASTID_OP_AND>(rv, qv);
                         }
                 }
             }
@@ -360,7 +370,7 @@ inline size_t scan_smem_bytes(const CompareArgs& a, int kpad) {
 template <int MODE, int KP, int QN>
 int launch_scan_q(const CompareArgs& a, int n_ctas, cudaStream_t stream) {
     const size_t smem = scan_smem_bytes(a, KP);
-    auto kern = popc_scan_kernel<MODE, KP, QN>;
+    auto kern = a.op == FASTID_OP_XOR ? popc_scan_kernel<MODE, KP, QN, true> : popc_scan_kernel<MODE, KP, QN, false>;
     FASTID_CUDA(ensure_dynamic_smem((const void*)kern, (int)smem));
     kern<<<(unsigned)n_ctas, 32 * kScanWarps, smem, stream>>>(a);
     FASTID_LAUNCHED("popc_scan_kernel");
@@ -383,7 +393,9 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     const int64_t n_ref_tiles = ceil_div(a.n_refs, kRows);
     const int64_t n_q_tiles = ceil_div(a.n_queries, kRows);
     size_t smem = kStages * kStageBytes + (MODE == kTopK ? kRows * kScorePitch * 4 : 0);
-    auto kern = popc_kernel<MODE, KP>;
+    auto kern = a.op == FASTID_OP_AND   ? popc_kernel<MODE, KP, FASTID_OP_AND>
+                : a.op == FASTID_OP_XOR ? popc_kernel<MODE, KP, FASTID_OP_XOR>
+                                        : popc_kernel<MODE, KP, FASTID_OP_ANDNOT>;
     FASTID_CUDA(ensure_dynamic_smem((const void*)kern, (int)smem));
     dim3 grid;
     if (MODE == kTopK) {
@@ -397,7 +409,33 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     return FASTID_OK;
 }
 
+// One warp per row: the row's popcount (XOR scores on the tensor path).
+__global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n, int64_t stride,
+                                    uint32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int n16 = (int)(stride / 16);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
+        const uint4* row = reinterpret_cast<const uint4*>(rows + r * stride);
+        uint32_t c = 0;
+        for (int i = lane; i < n16; i += 32) {
+            const uint4 v = __ldg(row + i);
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) out[r] = c;
+    }
+}
+
 }  // namespace
+
+int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, uint32_t* out, cudaStream_t stream) {
+    if (n <= 0) return FASTID_OK;
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 8);
+    row_popcount_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n, stride, out);
+    FASTID_LAUNCHED("row_popcount_kernel");
+    return FASTID_OK;
+}
 
 int popc_parts(int64_t n_refs, int64_t n_queries) {
     // Enough (group, slice) CTAs for ~2 waves at 2 CTAs/SM, and at most one

@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                     uint4 v = make_uint4(0, 0, 0, 0);
                     if (real && w4 < row_words) {
                         v = *reinterpret_cast<const uint4*>(src + w4);
-                        v = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
+                        if (a.op == FASTID_OP_ANDNOT) v = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
                     }
                     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -946,6 +946,11 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         // the k-th smallest published minimum is folded into a.bound by every list
         // at tiles 1, 2, 4, ... and then every 256th (SIMT-parallel over lanes)
         const uint32_t hit_bits = MODE == kThreshold ? score_bits<F>(a.threshold) : 0u;
+        // XOR: the MMA counts shared ones (A = the unknown rows as they are) and
+        // popc(r ^ q) = popc(r) + popc(q) - 2 popc(r & q) is formed here, before any
+        // compare, so every mode ranks and stores Hamming distances
+        const bool xor_op = a.op == FASTID_OP_XOR;
+        const uint32_t pq = xor_op && q_ok ? a.query_popc[q] : 0u;
         uint32_t t_empty_leader[kAccBufs] = {};
         if (PAIR) {
 #pragma unroll
@@ -976,6 +981,15 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             const int rl = !q_ok ? 0 : (rows_left >= kCols ? kCols : (rows_left > 0 ? (int)rows_left : 0));
             const bool full = rl == kCols;
             const uint32_t col_base = (uint32_t)(acc * BN + split * kCols);
+            auto to_xor = [&](uint32_t(&v)[kBatch], int b0) {
+                const int64_t rl_lane = r0 + b0 + lane;
+                const uint32_t pr_lane = rl_lane < a.n_refs ? __ldg(a.ref_popc + rl_lane) : 0u;
+#pragma unroll
+                for (int c = 0; c < kBatch; ++c) {
+                    const uint32_t pr = __shfl_sync(0xffffffffu, pr_lane, c);
+                    v[c] = score_bits<F>(pr + pq - 2u * decode_exact<F>(v[c]));
+                }
+            };
             // per-batch processing of up to 32 columns already in registers
             auto process = [&](uint32_t(&v)[kBatch], int b0, int nb) {
                 const int left = rl - b0;
@@ -1078,6 +1092,10 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 release();
+                if (xor_op) {
+#pragma unroll
+                    for (int b = 0; b < kPreBatches; ++b) to_xor(v[b], b * kBatch);
+                }
                 if (PAIR && MODE == kFull && a.tma_out == 2) {
                     // full matrix, wide: the 4 lane-quadrant warps of this column split fill
                     // one [kCols known rows][128 unknowns] block (512-B output rows) and one
@@ -1157,6 +1175,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && b0 == 0 && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 if (b0 + kBatch >= kCols) release();
+                if (xor_op) to_xor(v, b0);
                 process(v, b0, nb);
             }
             }
@@ -1370,7 +1389,10 @@ __global__ void prep_a_kernel(CompareArgs a, int n_groups, int n_kst, uint8_t* _
         for (int w = 0; w < kWordsPerStage; ++w) {
             const int word = ks * kWordsPerStage + w;
             uint32_t x = 0;
-            if (real && word < row_words) x = ~reinterpret_cast<const uint32_t*>(a.queries + q * a.stride)[word];
+            if (real && word < row_words) {
+                x = reinterpret_cast<const uint32_t*>(a.queries + q * a.stride)[word];
+                if (a.op == FASTID_OP_ANDNOT) x = ~x;
+            }
             if (F == FASTID_TENSOR_F4) {
                 *reinterpret_cast<uint4*>(dst + core_off(row, w, kM)) =
                     a.image && uniform_image(a) ? unpack_f4_uniform(x) : unpack_f4<false>(x);
@@ -1482,6 +1504,18 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     uint8_t* a_global = nullptr;
     CUtensorMap amap;
     memset(&amap, 0, sizeof(amap));
+    if (a.op == FASTID_OP_XOR) {
+        if (!a.ref_popc) {
+            auto* pr = (uint32_t*)launch_scratch(2, (size_t)a.n_refs * sizeof(uint32_t), stream);
+            if (!pr) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)a.n_refs);
+            if (int rc = launch_row_popcount(a.refs, a.n_refs, a.stride, pr, stream)) return rc;
+            a.ref_popc = pr;
+        }
+        auto* pq = (uint32_t*)launch_scratch(3, (size_t)a.n_queries * sizeof(uint32_t), stream);
+        if (!pq) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)a.n_queries);
+        if (int rc = launch_row_popcount(a.queries, a.n_queries, a.stride, pq, stream)) return rc;
+        a.query_popc = pq;
+    }
     if (SA) {
         const size_t bytes = (size_t)groups * lay.n_kst * Layout<F>::kAStageBytes;
         a_global = (uint8_t*)launch_scratch(0, bytes, stream);

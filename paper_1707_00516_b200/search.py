@@ -44,15 +44,16 @@ class PreparedImage:
     unpacking.  Built once per database (fastid_db_create).
     """
 
-    def __init__(self, panel: DevicePanel, formulation: str | int):
+    def __init__(self, panel: DevicePanel, formulation: str | int, op: str = "andnot"):
         from . import _native
 
         self.panel = panel  # keeps the packed rows alive for the handle
+        self.op = op
         self.handle = ctypes.c_void_p()
         L = _native.lib()
         with torch.cuda.device(panel.device):
             _native.check(L.fastid_db_create(panel.rows.data_ptr() if panel.n_profiles else 0, panel.n_profiles,
-                                             panel.stride, panel.bit_length, _native.formulation_code(formulation),
+                                             panel.stride, panel.bit_length, _native.formulation_code(formulation, op),
                                              torch.cuda.current_stream(panel.device).cuda_stream,
                                              ctypes.byref(self.handle)), "fastid_db_create")
         self.formulation = L.fastid_db_formulation(self.handle)
@@ -126,12 +127,14 @@ class ChunkedImage:
     index) order, full-matrix rows and threshold hits by row range).
     """
 
-    def __init__(self, panel: DevicePanel, formulation: str | int, chunk_rows: int | None = None):
+    def __init__(self, panel: DevicePanel, formulation: str | int, chunk_rows: int | None = None,
+                 op: str = "andnot"):
         from . import _native
         from .errors import DeviceError
 
         L = _native.lib()
         self.panel = panel
+        self.op = op
         code = _native.formulation_code(formulation)
         if code == 0:  # auto: the tensor formulation that runs this length
             code = _native.FORMULATIONS["tensor_f4"] if _native.supports("tensor_f4", panel.bit_length) else 1
@@ -177,13 +180,14 @@ class ChunkedImage:
             h = ctypes.c_void_p()
             with torch.cuda.device(self.panel.device):
                 _native.check(L.fastid_db_create_in(
-                    sub.rows.data_ptr(), nr, sub.stride, sub.bit_length, self.code, self.buf.data_ptr(),
+                    sub.rows.data_ptr(), nr, sub.stride, sub.bit_length, self.code | _native.operator_code(self.op),
+                    self.buf.data_ptr(),
                     self.buf.numel(), torch.cuda.current_stream(self.panel.device).cuda_stream, ctypes.byref(h)),
                     "fastid_db_create_in")
             for name, bit in DB_OPTIONS.items():
                 if self._bits & bit:
                     _native.check(L.fastid_db_set_option(h, bit, 1), "fastid_db_set_option")
-            view = _ChunkView(h)
+            view = _ChunkView(h, self.op)
             try:
                 yield r0, nr, sub, view
             finally:
@@ -209,8 +213,9 @@ PACKED_MAX_QUERIES = 128
 class _ChunkView:
     """A chunk's fastid_db handle, shaped like PreparedImage for the compare helpers."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, op: str):
         self.handle = handle
+        self.op = op
 
 
 class GraphedSearch:
@@ -286,7 +291,8 @@ class KnownDatabase:
     """A known panel resident on one device (or one shard of it, ``ref_base`` = global offset)."""
 
     def __init__(self, refs, bit_length: int | None = None, device=None, ref_base: int = 0,
-                 formulation: str | int = "auto", prepare: bool = True, image_chunk_rows: int | None = None):
+                 formulation: str | int = "auto", prepare: bool = True, image_chunk_rows: int | None = None,
+                 op: str = "andnot"):
         self.device = _require_cuda(device)
         if isinstance(refs, DevicePanel):
             self.panel = refs
@@ -298,6 +304,10 @@ class KnownDatabase:
             self.panel = DevicePanel.from_words(refs, bit_length, device=self.device)
         self.ref_base = int(ref_base)
         self.formulation = formulation
+        from . import _native
+
+        _native.operator_code(op)
+        self.op = op  # the bitwise operator of every search (compare_device's op)
         self._stagers: dict = {}
         # the tensor image (built once) lets every query batch skip bit unpacking; a
         # database whose image does not fit in device memory (4 bits per locus for
@@ -309,7 +319,7 @@ class KnownDatabase:
         if prepare and self.panel.n_profiles:
             # image_chunk_rows: build the image chunk by chunk into one buffer of that
             # many rows (what a panel whose whole image does not fit falls back to)
-            self.image = (ChunkedImage(self.panel, formulation, image_chunk_rows) if image_chunk_rows
+            self.image = (ChunkedImage(self.panel, formulation, image_chunk_rows, op) if image_chunk_rows
                           else self._prepare(formulation))
 
     def _prepare(self, formulation):
@@ -317,7 +327,7 @@ class KnownDatabase:
 
         for attempt in range(2):
             try:
-                return PreparedImage(self.panel, formulation)
+                return PreparedImage(self.panel, formulation, self.op)
             except DeviceError as e:
                 if "allocate" not in str(e):
                     raise
@@ -325,7 +335,7 @@ class KnownDatabase:
                     torch.cuda.empty_cache()  # cached torch blocks may be what is missing
                     continue
                 try:
-                    return ChunkedImage(self.panel, formulation)
+                    return ChunkedImage(self.panel, formulation, op=self.op)
                 except DeviceError as e2:
                     import warnings
 
@@ -368,15 +378,17 @@ class KnownDatabase:
             if n_q <= self.scan_max_queries:
                 # a handful of unknowns: the CUDA-core scan over the packed rows (HBM-bound)
                 # beats streaming the 4-bit image (one unknown, 20M x 1024 loci: 0.70 vs 1.52 ms)
-                return topk_device(self.panel, queries, k, max_score, self.ref_base, "popc", workspace, out)
+                return topk_device(self.panel, queries, k, max_score, self.ref_base, "popc", workspace, out,
+                                   op=self.op)
             if n_q <= self.packed_max_queries:
                 # one group of unknowns: the tensor kernel unpacking packed rows in shared
                 # memory reads 4x fewer bytes than the image and is faster
-                return topk_device(self.panel, queries, k, max_score, self.ref_base, "tensor_f4", workspace, out)
+                return topk_device(self.panel, queries, k, max_score, self.ref_base, "tensor_f4", workspace, out,
+                                   op=self.op)
         if self._chunked_for(queries.n_profiles):
             return self._topk_chunked(queries, k, max_score, workspace, out)
         return topk_device(self.panel, queries, k, max_score, self.ref_base, self.formulation, workspace, out,
-                           events=events, image=self._plain_image())
+                           events=events, image=self._plain_image(), op=self.op)
 
     def _topk_chunked(self, queries: DevicePanel, k: int, max_score, workspace, out):
         """Per chunk: its image, the fused top-k with the chunk's row offset, and a merge
@@ -397,7 +409,8 @@ class KnownDatabase:
         first = True
         for r0, nr, sub, view in self.image.chunks():
             dst = (cand_s[0], cand_x[0]) if first else (cand_s[1], cand_x[1])
-            topk_device(sub, queries, k, max_score, self.ref_base + r0, self.formulation, workspace, dst, image=view)
+            topk_device(sub, queries, k, max_score, self.ref_base + r0, self.formulation, workspace, dst, image=view,
+                        op=self.op)
             if not first:
                 with torch.cuda.device(dev):
                     _native.check(L.fastid_merge_topk(cand_s.data_ptr(), cand_x.data_ptr(), 2, n_q, k, k,
@@ -416,9 +429,9 @@ class KnownDatabase:
             if out is None:
                 out = torch.empty((self.panel.n_profiles, queries.n_profiles), dtype=torch.int32, device=self.device)
             for r0, nr, sub, view in self.image.chunks():
-                compare_device(sub, queries, out[r0:r0 + nr], self.formulation, image=view)
+                compare_device(sub, queries, out[r0:r0 + nr], self.formulation, image=view, op=self.op)
             return out
-        return compare_device(self.panel, queries, out, self.formulation, image=self._plain_image())
+        return compare_device(self.panel, queries, out, self.formulation, image=self._plain_image(), op=self.op)
 
     # -- host-buffer public calls ------------------------------------------------
     def stager(self, n_queries: int, k: int, slot: int = 0) -> QueryStager:
@@ -532,15 +545,15 @@ class KnownDatabase:
             if n_q <= self.scan_max_queries:
                 # a handful of unknowns: the CUDA-core scan over the packed rows
                 return threshold_hits(self.panel, queries, threshold, capacity, "popc", self.device,
-                                      ref_base=self.ref_base)
+                                      ref_base=self.ref_base, op=self.op)
             if n_q <= self.packed_max_queries:
                 # one group of unknowns: packed rows unpacked in shared memory beat the image
                 # (20M x 1024 loci, 32-128 unknowns: 1.26 vs 1.61 ms; 5M x 5000: 1.71-1.73 vs 2.01-2.04)
                 return threshold_hits(self.panel, queries, threshold, capacity, "tensor_f4", self.device,
-                                      ref_base=self.ref_base)
+                                      ref_base=self.ref_base, op=self.op)
         if self._chunked_for(n_q):
             parts = [threshold_hits(sub, queries, threshold, capacity, self.formulation, self.device,
-                                    ref_base=self.ref_base + r0, image=view)
+                                    ref_base=self.ref_base + r0, image=view, op=self.op)
                      for r0, nr, sub, view in self.image.chunks()]
             q = np.concatenate([h.query for h in parts])
             r = np.concatenate([h.ref for h in parts])
@@ -548,4 +561,4 @@ class KnownDatabase:
             order = np.lexsort((r, q))
             return ThresholdHits(q[order], r[order], sc[order], int(threshold))
         return threshold_hits(self.panel, queries, threshold, capacity, self.formulation, self.device,
-                              ref_base=self.ref_base, image=self._plain_image())
+                              ref_base=self.ref_base, image=self._plain_image(), op=self.op)
