@@ -124,3 +124,22 @@ def test_known_database_options_are_named():
     from paper_1707_00516_b200.search import DB_OPTIONS
 
     assert DB_OPTIONS == {"no_cta_pairs": 1, "no_tma_store": 2, "no_spare_pairs": 4, "narrow_tma_store": 8}
+
+
+def test_operator_codes_and_validation():
+    """op= maps to the C ABI's operator bits (include/fastid_b200.h); unknown
+    operators are rejected before any device work, by Python and by the library."""
+    from paper_1707_00516_b200 import _native
+
+    assert _native.formulation_code("tensor_f4") == 3
+    assert _native.formulation_code("tensor_f4", "and") == 3 | 0x100
+    assert _native.formulation_code(1, "xor") == 1 | 0x200
+    with pytest.raises(ValueError):
+        _native.formulation_code("auto", "nand")
+    L = _native.lib()
+    assert L.fastid_supports(3 | 0x200, 1024) == 1
+    assert L.fastid_supports(0x300, 1024) == 0  # no such operator
+    assert L.fastid_db_set_operator(None, 0) == _native.E_INVALID
+    a = fb.Panel(("a",), np.zeros((1, 1), np.uint64), 64)
+    with pytest.raises(ValueError):
+        fb.compare_b200(a, a, op="or")

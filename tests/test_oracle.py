@@ -146,3 +146,20 @@ def test_fidm_format_matches_reference_files():
     for name in ("golden_4x4", "rand_37x23_L100"):
         r, q = d[f"{name}__refs"], d[f"{name}__queries"]
         assert fidm_bytes(oracle.naive(r, q)) == d[f"{name}__fidm"].tobytes(), name
+
+
+def test_operator_restatements(rng):
+    """np_scores_op: "andnot" is Eq. 1 (== the pinned C oracle); "and" / "xor"
+    follow their definitions and the identity the tensor epilogue uses
+    (xor = popc(r) + popc(q) - 2 and).  AND and XOR are parity-unpinned
+    extensions (the reference computes AND-NOT only)."""
+    r, _ = rand_words(rng, 70, 5, 64, 300)
+    q, _ = rand_words(rng, 9, 5, 64, 300)
+    assert np.array_equal(oracle.np_scores_op(r, q, "andnot"), oracle.naive(r, q))
+    both = oracle.np_scores_op(r, q, "and", block=16).astype(np.int64)
+    pr = np.bitwise_count(r).sum(axis=1, dtype=np.int64)
+    pq = np.bitwise_count(q).sum(axis=1, dtype=np.int64)
+    assert np.array_equal(oracle.np_scores_op(r, q, "xor"), pr[:, None] + pq[None, :] - 2 * both)
+    assert np.array_equal(oracle.np_scores_op(r, q, "andnot").astype(np.int64), pr[:, None] - both)
+    with pytest.raises(KeyError):
+        oracle.np_scores_op(r, q, "or")
