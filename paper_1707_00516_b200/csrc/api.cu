@@ -668,19 +668,23 @@ extern "C" int fastid_db_set_operator(fastid_db* db, int op) {
 }
 
 namespace {
-// XOR on the image: the rows' popcounts, computed once per handle on the first XOR call
+// XOR on the i8 image: the rows' popcounts, computed once per handle on the first XOR
+// call (the mxf4 kernels fold them into the MMA, tensor.cu unpack_f4_xor)
 int db_ref_popc(fastid_db* db, void* stream, const uint32_t** out) {
     *out = nullptr;
-    if (db->op != FASTID_OP_XOR || db->formulation == FASTID_POPC || db->n_refs == 0) return FASTID_OK;
+    if (db->op != FASTID_OP_XOR || db->formulation != FASTID_TENSOR_I8 || db->n_refs == 0) return FASTID_OK;
     if (!db->ref_popc) {
-        if (cudaMalloc(&db->ref_popc, (size_t)db->n_refs * sizeof(uint32_t)) != cudaSuccess) {
+        if (cudaMalloc(&db->ref_popc, (size_t)popcount_entries(db->n_refs) * sizeof(uint32_t)) != cudaSuccess) {
             cudaGetLastError();
             db->ref_popc = nullptr;
             FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)db->n_refs);
         }
-        if (int rc = launch_row_popcount((const uint8_t*)db->refs, db->n_refs, db->stride, db->ref_popc,
-                                         (cudaStream_t)stream))
+        if (int rc = launch_row_popcount((const uint8_t*)db->refs, db->n_refs, db->stride,
+                                         db->formulation == FASTID_TENSOR_F4, db->ref_popc, (cudaStream_t)stream))
             return rc;
+        // later calls may come on other streams: the cache is complete before it is shared
+        if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+            FASTID_FAIL(FASTID_E_CUDA, "row popcounts: %s", cudaGetErrorString(cudaGetLastError()));
     }
     *out = db->ref_popc;
     return FASTID_OK;

@@ -244,8 +244,13 @@ int launch_tensor(Mode mode, const CompareArgs& a, int formulation, int* n_parts
 int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation);
 int tensor_supported(int64_t bit_length, int formulation);
 size_t tensor_image_bytes(int64_t n_refs, int64_t bit_length, int formulation);
-// popcount of each of `n` rows of `stride` bytes -> out[n] (u32), on `stream`
-int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, uint32_t* out, cudaStream_t stream);
+// popcount of each of `n` rows of `stride` bytes -> out[n] (u32, or the fp32 bits
+// of the count when `as_float`: the mxf4 epilogue's XOR transform), on `stream`
+int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, bool as_float, uint32_t* out,
+                        cudaStream_t stream);
+// entries of a known-row popcount buffer: n rounded up to whole 256-row tiles
+// (the XOR epilogue reads a full 32-column batch past the last row)
+inline int64_t popcount_entries(int64_t n) { return (n + 255) / 256 * 256; }
 int build_tensor_image(const CompareArgs& a, int formulation, void* image, cudaStream_t stream);
 int launch_merge(const uint32_t* cand_scores, const int64_t* cand_index, int n_lists,
                  int64_t n_queries, int k_in, int k, uint32_t* top_scores, int64_t* top_index,

@@ -410,7 +410,7 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
 }
 
 // One warp per row: the row's popcount (XOR scores on the tensor path).
-__global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n, int64_t stride,
+__global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n, int64_t stride, bool as_float,
                                     uint32_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
@@ -423,16 +423,17 @@ __global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n,
             c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
         }
         c = __reduce_add_sync(0xffffffffu, c);
-        if (lane == 0) out[r] = c;
+        if (lane == 0) out[r] = as_float ? __float_as_uint((float)c) : c;
     }
 }
 
 }  // namespace
 
-int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, uint32_t* out, cudaStream_t stream) {
+int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, bool as_float, uint32_t* out,
+                        cudaStream_t stream) {
     if (n <= 0) return FASTID_OK;
     const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 8);
-    row_popcount_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n, stride, out);
+    row_popcount_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n, stride, as_float, out);
     FASTID_LAUNCHED("row_popcount_kernel");
     return FASTID_OK;
 }

@@ -150,6 +150,28 @@ __device__ __forceinline__ uint4 unpack_f4(uint32_t w) {
 __device__ __forceinline__ uint4 unpack_f4_uniform(uint32_t w) {
     return make_uint4((w & 0x11111111u) << 1, w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
 }
+// XOR on mxf4: the unknown side is +1 for a clear bit and -1 (e2m1 sign 0x8) for a
+// set bit, so the MMA sums r_k (1 - 2 q_k) = popc(r) - 2 popc(r & q) and the
+// epilogue adds popc(q): popc(r ^ q) with one FADD and no known-row popcounts.
+// Each component of the unpacked words holds its bit at one nibble position
+// (uniform: bit 1; weighted A side: bits 2, 1, 0, 0), shifted up to bit 3.
+__device__ __forceinline__ uint4 unpack_f4_xor(uint32_t w, bool uniform) {
+    if (uniform) {
+        const uint4 s = unpack_f4_uniform(w);
+        return make_uint4(0x22222222u | s.x << 2, 0x22222222u | s.y << 2, 0x22222222u | s.z << 2,
+                          0x22222222u | s.w << 2);
+    }
+    const uint4 s = unpack_f4<false>(w);
+    return make_uint4(0x44444444u | s.x << 1, 0x22222222u | s.y << 2, 0x11111111u | s.z << 3,
+                      0x11111111u | s.w << 3);
+}
+// The A-side nibbles of one word of unknown bits (already complemented for AND-NOT);
+// zero outside the row.
+__device__ __forceinline__ uint4 unpack_a_f4(uint32_t w, bool uniform, bool xor_op, bool in_row) {
+    if (xor_op) return in_row ? unpack_f4_xor(w, uniform) : make_uint4(0, 0, 0, 0);
+    return uniform ? unpack_f4_uniform(w) : unpack_f4<false>(w);
+}
+
 // The producer waits for ring slots with a suspend-time hint (it runs stages
 // ahead of the MMA, so its wake-up latency is hidden; sleeping instead of
 // re-issuing try_wait lowers power under the cap): ~1% on C3.
@@ -806,8 +828,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         // Resident A = complemented unknown rows of one segment's group; zero
         // past the row.  Threads 0..127 of the builder warps each build one row.
         auto build_a = [&](int64_t q0s) {
-            // Resident A = complemented unknown rows; zero past the row.  Threads
-            // 0..127 each build one row.
+            // Resident A = the unknown rows (complemented for AND-NOT, +-1 for XOR);
+            // zero past the row.  Threads 0..127 each build one row.
             if (!SA && ct < kM) {
                 const int64_t q = q0s + ct;
                 const bool real = q < a.n_queries;
@@ -815,7 +837,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(a.queries + (real ? q : 0) * a.stride);
                 for (int w4 = 0; w4 < n_kst * kWordsPerStage; w4 += 4) {
                     uint4 v = make_uint4(0, 0, 0, 0);
-                    if (real && w4 < row_words) {
+                    const bool in_row = real && w4 < row_words;
+                    if (in_row) {
                         v = *reinterpret_cast<const uint4*>(src + w4);
                         if (a.op == FASTID_OP_ANDNOT) v = make_uint4(~v.x, ~v.y, ~v.z, ~v.w);
                     }
@@ -825,7 +848,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                         const int col = (w4 + i) * CPW;
                         if (F == FASTID_TENSOR_F4) {
                             *reinterpret_cast<uint4*>(sA + core_off(ct, col, kM)) =
-                                IMG && uniform_image(a) ? unpack_f4_uniform(wv[i]) : unpack_f4<false>(wv[i]);
+                                unpack_a_f4(wv[i], IMG && uniform_image(a), a.op == FASTID_OP_XOR, in_row);
                         } else {
                             uint4 lo, hi;
                             unpack_i8<false>(wv[i], lo, hi);
@@ -949,6 +972,9 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         // XOR: the MMA counts shared ones (A = the unknown rows as they are) and
         // popc(r ^ q) = popc(r) + popc(q) - 2 popc(r & q) is formed here, before any
         // compare, so every mode ranks and stores Hamming distances
+        // (mxf4: the MMA already holds popc(r) - 2 popc(r & q), see unpack_f4_xor, and
+        // popc(q) is stored as fp32 bits: one exact FADD per value; i8: the integer
+        // identity with the known rows' popcounts)
         const bool xor_op = a.op == FASTID_OP_XOR;
         const uint32_t pq = xor_op && q_ok ? a.query_popc[q] : 0u;
         uint32_t t_empty_leader[kAccBufs] = {};
@@ -982,17 +1008,43 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
             const bool full = rl == kCols;
             const uint32_t col_base = (uint32_t)(acc * BN + split * kCols);
             auto to_xor = [&](uint32_t(&v)[kBatch], int b0) {
-                const int64_t rl_lane = r0 + b0 + lane;
-                const uint32_t pr_lane = rl_lane < a.n_refs ? __ldg(a.ref_popc + rl_lane) : 0u;
+                if constexpr (F == FASTID_TENSOR_F4) {
 #pragma unroll
-                for (int c = 0; c < kBatch; ++c) {
-                    const uint32_t pr = __shfl_sync(0xffffffffu, pr_lane, c);
-                    v[c] = score_bits<F>(pr + pq - 2u * decode_exact<F>(v[c]));
+                    for (int c = 0; c < kBatch; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) + __uint_as_float(pq));
+                    return;
+                }
+                // the batch's 32 row popcounts: warp-uniform 16-byte loads (the buffer is
+                // padded past n_refs to whole tiles; padding columns are discarded)
+                const uint4* p4 = reinterpret_cast<const uint4*>(a.ref_popc + r0 + b0);
+#pragma unroll
+                for (int c4 = 0; c4 < kBatch / 4; ++c4) {
+                    const uint4 p = __ldg(p4 + c4);
+                    const uint32_t pc[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int c = c4 * 4 + i;
+                        v[c] = score_bits<F>(pc[i] + pq - 2u * decode_exact<F>(v[c]));
+                    }
                 }
             };
             // per-batch processing of up to 32 columns already in registers
             auto process = [&](uint32_t(&v)[kBatch], int b0, int nb) {
                 const int left = rl - b0;
+                if constexpr (F == FASTID_TENSOR_F4 && MODE != kFull) {
+                    if (xor_op) {
+                        // popc(q) is one constant per lane (unknown): the batch's minimum
+                        // decides in the raw domain (fp32 min, the same cost as the integer
+                        // min of AND-NOT) and only a batch that can insert or hit pays for
+                        // the per-value FADD (warp-uniform skip)
+                        float mn = __uint_as_float(v[0]);
+#pragma unroll
+                        for (int c = 1; c < kBatch; ++c) mn = fminf(mn, __uint_as_float(v[c]));
+                        const uint32_t mb = __float_as_uint(mn + __uint_as_float(pq));
+                        const bool need = left > 0 && (MODE == kTopK ? mb < thr_eff : mb <= hit_bits);
+                        if (!__any_sync(0xffffffffu, need)) return;
+                        to_xor(v, b0);
+                    }
+                }
                 const uint32_t valid = full || left >= kBatch ? (nb == 32 ? 0xFFFFFFFFu : (1u << nb) - 1u)
                                                               : (left <= 0 ? 0u : (1u << left) - 1u);
                 const int64_t rc = r0 + b0;
@@ -1092,7 +1144,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 release();
-                if (xor_op) {
+                if (xor_op && (MODE == kFull || F != FASTID_TENSOR_F4)) {
 #pragma unroll
                     for (int b = 0; b < kPreBatches; ++b) to_xor(v[b], b * kBatch);
                 }
@@ -1175,7 +1227,7 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                 }
                 if (tr && b0 == 0 && !experiment(a, 8)) trace_buf(a)[local * kTrSlots + kTrB0Loaded + ew] = clock64();
                 if (b0 + kBatch >= kCols) release();
-                if (xor_op) to_xor(v, b0);
+                if (xor_op && (MODE == kFull || F != FASTID_TENSOR_F4)) to_xor(v, b0);
                 process(v, b0, nb);
             }
             }
@@ -1395,7 +1447,7 @@ __global__ void prep_a_kernel(CompareArgs a, int n_groups, int n_kst, uint8_t* _
             }
             if (F == FASTID_TENSOR_F4) {
                 *reinterpret_cast<uint4*>(dst + core_off(row, w, kM)) =
-                    a.image && uniform_image(a) ? unpack_f4_uniform(x) : unpack_f4<false>(x);
+                    unpack_a_f4(x, a.image && uniform_image(a), a.op == FASTID_OP_XOR, real && word < row_words);
             } else {
                 uint4 lo, hi;
                 unpack_i8<false>(x, lo, hi);
@@ -1505,15 +1557,18 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
     CUtensorMap amap;
     memset(&amap, 0, sizeof(amap));
     if (a.op == FASTID_OP_XOR) {
-        if (!a.ref_popc) {
-            auto* pr = (uint32_t*)launch_scratch(2, (size_t)a.n_refs * sizeof(uint32_t), stream);
-            if (!pr) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)a.n_refs);
-            if (int rc = launch_row_popcount(a.refs, a.n_refs, a.stride, pr, stream)) return rc;
+        constexpr bool kFloat = F == FASTID_TENSOR_F4;
+        if (kFloat) a.ref_popc = nullptr;  // mxf4 needs only the unknowns' popcounts
+        if (!kFloat && !a.ref_popc) {
+            const size_t n = (size_t)popcount_entries(a.n_refs);
+            auto* pr = (uint32_t*)launch_scratch(2, n * sizeof(uint32_t), stream);
+            if (!pr) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %zu row popcounts", n);
+            if (int rc = launch_row_popcount(a.refs, a.n_refs, a.stride, kFloat, pr, stream)) return rc;
             a.ref_popc = pr;
         }
         auto* pq = (uint32_t*)launch_scratch(3, (size_t)a.n_queries * sizeof(uint32_t), stream);
         if (!pq) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)a.n_queries);
-        if (int rc = launch_row_popcount(a.queries, a.n_queries, a.stride, pq, stream)) return rc;
+        if (int rc = launch_row_popcount(a.queries, a.n_queries, a.stride, kFloat, pq, stream)) return rc;
         a.query_popc = pq;
     }
     if (SA) {
