@@ -205,6 +205,34 @@ __global__ void __launch_bounds__(kThreads, MODE == kTopK ? 1 : 2) popc_kernel(C
 // published), and inserts with one shuffle round.  At the end the CTA's warps'
 // lists are merged into one partial list per CTA, which the merge kernel folds
 // like any other partials.
+// Warp-wide (score, index) sort helpers of the scan's list update: one pair per lane.
+__device__ __forceinline__ void cmp_exchange(uint32_t& s, uint32_t& x, int d, bool keep_min) {
+    const uint32_t os = __shfl_xor_sync(0xFFFFFFFFu, s, d);
+    const uint32_t ox = __shfl_xor_sync(0xFFFFFFFFu, x, d);
+    if (keep_min ? before(os, ox, s, x) : before(s, x, os, ox)) {
+        s = os;
+        x = ox;
+    }
+}
+// ascending bitonic sort of the warp's 32 pairs
+__device__ __forceinline__ void warp_sort(uint32_t& s, uint32_t& x, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int d = k >> 1; d > 0; d >>= 1) cmp_exchange(s, x, d, ((lane & d) == 0) == ((lane & k) == 0));
+}
+// ascending sort of a bitonic sequence
+__device__ __forceinline__ void warp_bitonic_merge(uint32_t& s, uint32_t& x, int lane) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) cmp_exchange(s, x, d, (lane & d) == 0);
+}
+// A step with at least this many admissible rows merges them into the list at
+// once (sort + bitonic merge, ~21 shuffle rounds) instead of one insertion each
+// (~8 dependent shuffles per row): the first steps of every warp, whose lists
+// are still empty, admit all 32 rows.  Up to two unknowns per kernel (the
+// popcount-bound 4+-unknown instances ran 3-13% slower with the extra code).
+constexpr int kScanBulkMin = 4;
+
 constexpr int kScanMaxQ = 16;
 constexpr int kScanWarps = 8;
 constexpr int kScanPiece = 8;  // uint4 per row per staging round (128 B)
@@ -291,6 +319,30 @@ __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_ke
             if (j >= nq) break;
             const bool cand = valid && acc[j] <= gb[j] && before(acc[j], rl, ks[j], kx[j]);
             uint32_t m = __ballot_sync(0xFFFFFFFFu, cand);
+            if (QN <= 2 && __popc(m) >= kScanBulkMin) {
+                // the admissible rows, sorted; min against the reversed list gives the 32
+                // smallest of both as a bitonic sequence (lanes >= KP hold empty entries)
+                uint32_t bs = cand ? acc[j] : kEmptyScore, bx = cand ? rl : kEmptyLocal;
+                warp_sort(bs, bx, lane);
+                const uint32_t rs = __shfl_sync(0xFFFFFFFFu, bs, 31 - lane);
+                const uint32_t rx = __shfl_sync(0xFFFFFFFFu, bx, 31 - lane);
+                if (before(rs, rx, ls[j], lx[j])) {
+                    ls[j] = rs;
+                    lx[j] = rx;
+                }
+                warp_bitonic_merge(ls[j], lx[j], lane);
+                if (lane >= KP) {
+                    ls[j] = kEmptyScore;
+                    lx[j] = kEmptyLocal;
+                }
+                ks[j] = __shfl_sync(0xFFFFFFFFu, ls[j], KP - 1);
+                kx[j] = __shfl_sync(0xFFFFFFFFu, lx[j], KP - 1);
+                if (ks[j] < gb[j]) {
+                    gb[j] = ks[j];
+                    if (lane == 0) atomicMin(a.bound + j, ks[j]);
+                }
+                m = 0;
+            }
             while (m) {
                 const int src = __ffs(m) - 1;
                 m &= m - 1;
@@ -310,8 +362,11 @@ __global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_ke
                 }
                 ks[j] = __shfl_sync(0xFFFFFFFFu, ls[j], KP - 1);
                 kx[j] = __shfl_sync(0xFFFFFFFFu, lx[j], KP - 1);
-                if (ks[j] != kEmptyScore) {
-                    if (ks[j] < gb[j]) gb[j] = ks[j];
+                // publish only a list end that beats the bound this warp knows: an
+                // atomicMin at or above it changes nothing, and every warp hitting one
+                // address serialises in its L2 slice (one unknown, 2M rows: 199 us)
+                if (ks[j] < gb[j]) {
+                    gb[j] = ks[j];
                     if (lane == 0) atomicMin(a.bound + j, ks[j]);
                 }
             }
@@ -459,16 +514,28 @@ int launch_popc(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t stre
             return launch_scan<kThreshold, 8>(a, 4 * num_sms(), stream);
         return launch_mode<kThreshold, 1>(a, 1, stream);
     }
-    const int parts = popc_parts(a.n_refs, a.n_queries);
-    *n_parts = parts;
+    int parts = popc_parts(a.n_refs, a.n_queries);
     // few unknowns (and their rows, plus the merge lists, in shared memory): the scan
     if (a.n_queries <= kScanMaxQ && scan_smem_bytes(a, a.kpad) <= 200 * 1024) {
+        // one unknown: 3 CTAs per SM (fewer per-warp lists, fewer insertions) measured
+        // 0.535 vs 0.592 ms at 4 (20M x 1024 loci, tools/scan_timing.py); from two
+        // unknowns on, the popcount work wants the 4th CTA (4 unknowns: 1.20 vs 1.38 ms)
+        if (a.n_queries == 1) parts = std::min(parts, 3 * num_sms());
+        // FASTID_SCAN_CTAS: grid size of the scan (scheduling only; <= kMaxMergeLists)
+        if (const char* e = getenv("FASTID_SCAN_CTAS")) {
+            const int v = atoi(e);
+            // (never above the lists the workspace holds: fastid_topk_workspace)
+            if (v > 0 && v <= kMaxMergeLists && v <= std::max(parts, tensor_parts(a.n_refs, a.n_queries, FASTID_TENSOR_F4)))
+                parts = v;
+        }
+        *n_parts = parts;
         switch (a.kpad) {
             case 8: return launch_scan<kTopK, 8>(a, parts, stream);
             case 16: return launch_scan<kTopK, 16>(a, parts, stream);
             case 32: return launch_scan<kTopK, 32>(a, parts, stream);
         }
     }
+    *n_parts = parts;
     switch (a.kpad) {
         case 8: return launch_mode<kTopK, 8>(a, parts / 2, stream);
         case 16: return launch_mode<kTopK, 16>(a, parts / 2, stream);

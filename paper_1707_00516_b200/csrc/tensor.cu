@@ -1079,7 +1079,8 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
                                 const uint32_t kth = top.s[KP - 1];
                                 thr_bits = kth < cap_bits ? kth : cap_bits;
                                 if (thr_bits < thr_eff) thr_eff = thr_bits;
-                                if (share && kth != kEmptyScore) atomicMin(a.bound + q, kth + 1u);
+                                // (at or above the bound read this tile the atomic changes nothing)
+                                if (share && kth != kEmptyScore && kth + 1u < shared_bound) atomicMin(a.bound + q, kth + 1u);
                             }
                         }
                     }
