@@ -679,7 +679,7 @@ int db_ref_popc(fastid_db* db, void* stream, const uint32_t** out) {
             db->ref_popc = nullptr;
             FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)db->n_refs);
         }
-        if (int rc = launch_row_popcount((const uint8_t*)db->refs, db->n_refs, db->stride,
+        if (int rc = launch_row_popcount((const uint8_t*)db->refs, db->n_refs, popcount_entries(db->n_refs), db->stride,
                                          db->formulation == FASTID_TENSOR_F4, db->ref_popc, (cudaStream_t)stream))
             return rc;
         // later calls may come on other streams: the cache is complete before it is shared

@@ -245,8 +245,9 @@ int tensor_parts(int64_t n_refs, int64_t n_queries, int formulation);
 int tensor_supported(int64_t bit_length, int formulation);
 size_t tensor_image_bytes(int64_t n_refs, int64_t bit_length, int formulation);
 // popcount of each of `n` rows of `stride` bytes -> out[n] (u32, or the fp32 bits
-// of the count when `as_float`: the mxf4 epilogue's XOR transform), on `stream`
-int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, bool as_float, uint32_t* out,
+// of the count when `as_float`: the mxf4 epilogue's XOR transform), zeros in
+// out[n .. n_out), on `stream`
+int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t n_out, int64_t stride, bool as_float, uint32_t* out,
                         cudaStream_t stream);
 // entries of a known-row popcount buffer: n rounded up to whole 256-row tiles
 // (the XOR epilogue reads a full 32-column batch past the last row)

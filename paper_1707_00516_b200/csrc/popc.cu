@@ -465,12 +465,16 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
 }
 
 // One warp per row: the row's popcount (XOR scores on the tensor path).
-__global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n, int64_t stride, bool as_float,
-                                    uint32_t* __restrict__ out) {
+__global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n, int64_t n_out, int64_t stride,
+                                    bool as_float, uint32_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
     const int n16 = (int)(stride / 16);
-    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n_out; r += warps) {
+        if (r >= n) {  // padding entries: defined zeros
+            if (lane == 0) out[r] = 0;
+            continue;
+        }
         const uint4* row = reinterpret_cast<const uint4*>(rows + r * stride);
         uint32_t c = 0;
         for (int i = lane; i < n16; i += 32) {
@@ -484,11 +488,11 @@ __global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n,
 
 }  // namespace
 
-int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t stride, bool as_float, uint32_t* out,
+int launch_row_popcount(const uint8_t* rows, int64_t n, int64_t n_out, int64_t stride, bool as_float, uint32_t* out,
                         cudaStream_t stream) {
-    if (n <= 0) return FASTID_OK;
-    const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 8);
-    row_popcount_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n, stride, as_float, out);
+    if (n_out <= 0) return FASTID_OK;
+    const int64_t blocks = std::min<int64_t>(ceil_div(n_out, 8), (int64_t)num_sms() * 8);
+    row_popcount_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n, n_out, stride, as_float, out);
     FASTID_LAUNCHED("row_popcount_kernel");
     return FASTID_OK;
 }

@@ -1564,12 +1564,13 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
             const size_t n = (size_t)popcount_entries(a.n_refs);
             auto* pr = (uint32_t*)launch_scratch(2, n * sizeof(uint32_t), stream);
             if (!pr) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %zu row popcounts", n);
-            if (int rc = launch_row_popcount(a.refs, a.n_refs, a.stride, kFloat, pr, stream)) return rc;
+            if (int rc = launch_row_popcount(a.refs, a.n_refs, (int64_t)n, a.stride, kFloat, pr, stream)) return rc;
             a.ref_popc = pr;
         }
         auto* pq = (uint32_t*)launch_scratch(3, (size_t)a.n_queries * sizeof(uint32_t), stream);
         if (!pq) FASTID_FAIL(FASTID_E_NOMEM, "cannot allocate %lld row popcounts", (long long)a.n_queries);
-        if (int rc = launch_row_popcount(a.queries, a.n_queries, a.stride, kFloat, pq, stream)) return rc;
+        if (int rc = launch_row_popcount(a.queries, a.n_queries, a.n_queries, a.stride, kFloat, pq, stream))
+            return rc;
         a.query_popc = pq;
     }
     if (SA) {

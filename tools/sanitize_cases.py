@@ -103,6 +103,35 @@ def main():
     jj, ii = np.nonzero(expected.T <= thr)
     assert np.array_equal(hits.query, jj) and np.array_equal(hits.ref, ii), "scan threshold"
     n_cases += 2
+    # one and two unknowns: the scan's bulk (sort + merge) list updates
+    for nq in (1, 2):
+        res = fb.topk(refs, fb.Panel(queries.ids[:nq], queries.words[:nq], 777), 16, formulation="popc")
+        es, ex, _ = oracle.topk_from_matrix(expected[:, :nq], 16)
+        assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), ("scan bulk", nq)
+        n_cases += 1
+    # AND / XOR operators: tiled kernel, scan, tensor kernels (packed rows and the image,
+    # XOR's signed mxf4 operand and the i8 popcount epilogue)
+    for L, n_r, n_q in ((1024, 700, 40), (5000, 400, 3)):
+        refs, queries = panel(rng, n_r, L, "r"), panel(rng, n_q, L, "q")
+        for op in ("and", "xor"):
+            expected = oracle.np_scores_op(refs.words, queries.words, op)
+            es, ex, _ = oracle.topk_from_matrix(expected, 8)
+            for form in ("popc", "tensor_i8", "tensor_f4"):
+                if not fb._native.supports(form, L):
+                    continue
+                got = fb.compare_b200(refs, queries, formulation=form, op=op).scores
+                assert np.array_equal(got, expected), (L, op, form, "full")
+                res = fb.topk(refs, queries, 8, formulation=form, op=op)
+                assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), (L, op, form, "topk")
+                n_cases += 2
+            db = KnownDatabase(refs, op=op)
+            s, x = db.search_words(queries.words, 8)
+            assert np.array_equal(s, es) and np.array_equal(x, ex), (L, op, "image topk")
+            thr = int(np.percentile(expected, 2))
+            hits = db.threshold(queries, thr)
+            jj, ii = np.nonzero(expected.T <= thr)
+            assert np.array_equal(hits.query, jj) and np.array_equal(hits.ref, ii), (L, op, "image threshold")
+            n_cases += 2
     torch.cuda.synchronize()
     print(f"sanitize cases ok ({n_cases})")
 
