@@ -1603,8 +1603,13 @@ int launch_one_impl(const CompareArgs& a_in, int n_slices, cudaStream_t stream) 
             // 10.2 ms at 40 tiles vs 12.4 at 20 and 10.8 at 80; 512 unknowns 3.1 ms at 40 vs
             // 4.1 at the 13 tiles of the byte budget).  Dual-tile pairs (long tiles): the
             // byte budget (C4: 2 tiles, 16.1 ms vs 17.9 at 3 and 19.0 at 6).
+            // More than 8 unknown groups (> 2048 unknowns) pace more peers each, and the
+            // slowest of them sets the pace: twice the window, within the byte budget
+            // (8192 unknowns: 39.1 ms at 80 tiles vs 47.5 at 40; 4096: flat; tools/nq_scan.py).
             const int64_t window = kDriftWindowBytes / ((int64_t)n_slices * lay.n_kst * Layout<F>::kUnpackedStageBytes);
-            ap.drift_tiles = SA ? (int)std::min<int64_t>(kDriftTilesMax, std::max<int64_t>(2, window)) : kDriftTilesMax;
+            const int64_t resident = pgroups > 8 ? std::max<int64_t>(kDriftTilesMax, std::min<int64_t>(2 * kDriftTilesMax, window))
+                                                 : kDriftTilesMax;
+            ap.drift_tiles = SA ? (int)std::min<int64_t>(kDriftTilesMax, std::max<int64_t>(2, window)) : (int)resident;
             // L2 prefetch of the known-tile stream: off by default (it cost C3 / C4 power and
             // clock for ~1% on one unknown group); FASTID_L2_PREFETCH=1 turns it on
             ap.l2_prefetch = 0;
