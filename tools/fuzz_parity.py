@@ -1,6 +1,7 @@
 """Randomised parity sweep on the GPU: random shapes (log-uniform sizes, loci
 near tile / stage / word boundaries, u32 and u64 words), random formulations,
-database options, chunked images, k, score caps and epilogues, each result
+database options, chunked images, k, score caps, epilogues and operators
+(AND-NOT / AND / XOR; AND and XOR against oracle.np_scores_op), each result
 compared bit-exactly with the oracle.  Runs for SECONDS; prints every failure
 with its seed so it can be replayed.
 
@@ -59,7 +60,21 @@ def case(seed):
     chunk = None
     if form == "tensor_f4" and n_r > 400 and rng.random() < 0.2:
         chunk = int(192 * rng.integers(1, max(2, n_r // 192)))
-    db = KnownDatabase(r, L, formulation=form, ref_base=int(rng.integers(0, 3)) * 1000, image_chunk_rows=chunk)
+    op = str(rng.choice(["andnot", "andnot", "andnot", "and", "xor"]))
+    if op != "andnot" and n_r * n_q * r.shape[1] > 3e8:
+        op = "andnot"  # the numpy operator oracle is for small cases
+
+    def o_full():
+        if op == "andnot":
+            return oracle.blocked(r, np.ascontiguousarray(q.T), 64, 16, workers)
+        return oracle.np_scores_op(r, q, op, block=max(1, int(5e7 // max(1, n_q * r.shape[1]))))
+
+    def o_topk(k, ms):
+        if op == "andnot":
+            return oracle.topk(r, q, k, ms, workers)
+        return oracle.topk_from_matrix(o_full(), k, ms)
+
+    db = KnownDatabase(r, L, formulation=form, ref_base=int(rng.integers(0, 3)) * 1000, image_chunk_rows=chunk, op=op)
     if chunk:
         db.chunked_min_queries = 1
     for name in DB_OPTIONS:
@@ -71,27 +86,27 @@ def case(seed):
         cr = int(rng.integers(1, n_r + 1)) if rng.random() < 0.8 else 0
         R = m.Panel(tuple(range(n_r)), r, L)
         Q = m.Panel(tuple(range(n_q)), q, L)
-        res = m.topk_streamed(R, Q, k, formulation=form, chunk_rows=cr, ref_base=7)
-        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE, workers)
+        res = m.topk_streamed(R, Q, k, formulation=form, chunk_rows=cr, ref_base=7, op=op)
+        es, ex, _ = o_topk(k, 0xFFFFFFFE)
         ok = np.array_equal(res.scores, es) and np.array_equal(res.index, np.where(ex >= 0, ex + 7, -1))
-        return ok, f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} streamed chunk_rows={cr} k={k}"
+        return ok, f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} op={op} streamed chunk_rows={cr} k={k}"
     if mode == "graphed":
         k = int(rng.integers(1, 33))
         g = db.graphed_search(n_q, k)
         s, x = g.run(q)
-        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE, workers)
+        es, ex, _ = o_topk(k, 0xFFFFFFFE)
         ok = np.array_equal(s, es) and np.array_equal(x, np.where(ex >= 0, ex + db.ref_base, -1))
-        return ok, f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} chunk={chunk} graphed k={k}"
-    desc = f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} chunk={chunk} opts={sorted(getattr(db.image, 'options', set()) or [])} {mode}"
+        return ok, f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} op={op} chunk={chunk} graphed k={k}"
+    desc = f"seed {seed}: {n_r}x{n_q}x{L} w{width} {form} op={op} chunk={chunk} opts={sorted(getattr(db.image, 'options', set()) or [])} {mode}"
     base = db.ref_base
     if mode == "topk":
         k = int(rng.integers(1, 33))
         ms = None if rng.random() < 0.6 else int(rng.integers(0, max(1, L // 2)))
         s, x = db.search_words(q, k, ms)
-        es, ex, _ = oracle.topk(r, q, k, 0xFFFFFFFE if ms is None else ms, workers)
+        es, ex, _ = o_topk(k, 0xFFFFFFFE if ms is None else ms)
         ok = np.array_equal(s, es) and np.array_equal(x, np.where(ex >= 0, ex + base, -1))
         return ok, desc + f" k={k} max={ms}"
-    full = oracle.blocked(r, np.ascontiguousarray(q.T), 64, 16, workers)
+    full = o_full()
     if mode == "threshold":
         t = int(np.percentile(full, rng.uniform(0, 3))) if full.size else 0
         h = db.threshold(m.Panel(tuple(range(n_q)), q, L), t)
