@@ -162,3 +162,28 @@ def test_operator_image_mismatch_raises(rng):
         m.compare_device(db.panel, dq, image=db.image, op="and")
     with pytest.raises(ValueError):
         m.topk(m.Panel(tuple(range(500)), r, 1024), m.Panel(tuple(range(10)), q, 1024), 4, op="nand")
+
+
+@pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8"])
+def test_db_set_operator_switches_a_prepared_image(rng, form):
+    """fastid_db_set_operator on a live handle: the same image serves AND-NOT, XOR
+    (the i8 image computes and caches its known-row popcounts on first use) and
+    AND, call after call."""
+    m = fb()
+    from paper_1707_00516_b200 import _native
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1024
+    r, q = _case(rng, 7000, 300, L)
+    db = KnownDatabase(r, L, formulation=form)
+    db.packed_max_queries = db.scan_max_queries = 0  # keep every batch on the image
+    for op in ("andnot", "xor", "and", "xor", "andnot"):
+        _native.check(_native.lib().fastid_db_set_operator(db.image.handle, _native.OPERATORS[op]),
+                      "fastid_db_set_operator")
+        db.op = db.image.op = op
+        exp = oracle.np_scores_op(r, q, op)
+        s, x = db.search_words(q, 16)
+        es, ex, _ = oracle.topk_from_matrix(exp, 16)
+        assert np.array_equal(s, es) and np.array_equal(x, ex), op
+        full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+        assert np.array_equal(full, exp), op
