@@ -74,6 +74,9 @@ def parse_args(argv=None):
     p.add_argument("--loci", type=int, default=None)
     p.add_argument("--k", type=int, default=None)
     p.add_argument("--formulation", default="auto")
+    # the bitwise operator before the popcount: "andnot" is the reference's Eq. 1 (the
+    # headline); "and" / "xor" are the library's operator extensions (no reference arm)
+    p.add_argument("--op", choices=("andnot", "and", "xor"), default="andnot")
     p.add_argument("--seed", type=int, default=1707)
     p.add_argument("--cpu-sample-known", type=int, default=100_000)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -106,6 +109,7 @@ def config_dict(args, world):
         "loci": args.loci,
         "k": args.k,
         "formulation": args.formulation,
+        "operator": args.op,
         "parallelism": f"known-db sharded over {world} rank(s), unknowns replicated, NCCL all-gather of top-k",
         "l2": (f"no flush: the {args.n_known * -(-args.loci // 128) * 16 / 1e9:.2f} GB packed known database "
                "(and its larger tensor image) streamed every step exceeds the 126 MB L2"),
@@ -224,6 +228,10 @@ def cpu_reference_sample(args, reps=3, warmup=1, prefer_reference=True):
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
+        return 0
+    if args.op != "andnot":
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference computes AND-NOT only (kernel.py:33-35), "
+                          f"not {args.op}"}))
         return 0
     world = max(world, args.gpus)
     oracle = _oracle()
@@ -490,7 +498,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     db_upload_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    db = KnownDatabase(db_panel, device=dev, ref_base=start, formulation=formulation)
+    db = KnownDatabase(db_panel, device=dev, ref_base=start, formulation=formulation, op=args.op)
     torch.cuda.synchronize()
     db_prepare_s = time.perf_counter() - t0
     sharded = ShardedDatabase(db, args.n_known)
@@ -624,7 +632,7 @@ def run_b200(args):
             pick = (np.arange(args.n_unknown) if args.verify == "full"
                     else np.unique(np.linspace(0, args.n_unknown - 1, 64).astype(int)))
             t0 = time.perf_counter()
-            (es, ex, _), _ = oracle.scan(refs_all, qwords[pick], k)
+            (es, ex, _), _ = oracle.scan(refs_all, qwords[pick], k, op=args.op)
             verify_s = time.perf_counter() - t0
             ok = bool(np.array_equal(s_dev[pick], es) and np.array_equal(x_dev[pick], ex))
             verified = {"ok": ok, "unknowns": int(len(pick)), "knowns": int(refs_all.shape[0]),
@@ -700,6 +708,8 @@ def run_b200(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {k2: v for k2, v in cpu_reference_sample(args).items() if k2 != "seconds_per_rep"}
+        if args.op != "andnot":  # the reference path has one operator; same words, same byte work
+            line["cpu_baseline"]["note"] = f"the reference computes AND-NOT only; timed on AND-NOT, not {args.op}"
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

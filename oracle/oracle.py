@@ -61,6 +61,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_threshold.restype = i64
         L.oracle_scan.argtypes = [vp, i64, vp, i64, i64, i32, i32, u32, i32, u32, i32, vp, vp, vp, i64, vp, vp, vp]
         L.oracle_scan.restype = i64
+        L.oracle_scan_op.argtypes = L.oracle_scan.argtypes + [i32]
+        L.oracle_scan_op.restype = i64
         L.oracle_score_word.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         L.oracle_score_word.restype = u32
         _lib = L
@@ -152,12 +154,17 @@ def threshold(refs: np.ndarray, queries: np.ndarray, t: int, capacity: int | Non
     return hq[:m].copy(), hr[:m].copy(), hs[:m].copy(), int(n)
 
 
+_SCAN_OPS = {"andnot": 0, "and": 1, "xor": 2}
+
+
 def scan(refs: np.ndarray, queries: np.ndarray, k: int = 0, max_score: int = 0xFFFFFFFF,
-         threshold: int | None = None, capacity: int = 1 << 24, workers: int | None = None):
+         threshold: int | None = None, capacity: int = 1 << 24, workers: int | None = None, op: str = "andnot"):
     """Database-scale derivations with all host threads (oracle_scan): the top-k
     of ``topk`` (k > 0) and/or the hits of ``threshold``, over row ranges merged
     in row order.  Returns (scores, index, counts) for k > 0 (else None) and
-    (query, ref, score, total) when ``threshold`` is given (else None)."""
+    (query, ref, score, total) when ``threshold`` is given (else None).  ``op``
+    "and" / "xor" score popcount(r AND q) / popcount(r XOR q) instead of Eq. 1
+    (operator extensions without a reference implementation: parity unpinned)."""
     refs, queries = _words(refs), _words(queries)
     assert refs.dtype == queries.dtype and refs.shape[1] == queries.shape[1]
     nq = queries.shape[0]
@@ -170,9 +177,9 @@ def scan(refs: np.ndarray, queries: np.ndarray, k: int = 0, max_score: int = 0xF
     hq = np.zeros(max(cap, 1), dtype=np.uint32)
     hr = np.zeros(max(cap, 1), dtype=np.int64)
     hs = np.zeros(max(cap, 1), dtype=np.uint32)
-    n = lib().oracle_scan(_ptr(refs), refs.shape[0], _ptr(queries), nq, refs.shape[1], refs.dtype.itemsize * 8,
-                          k, max_score, int(want), int(threshold or 0), workers or os.cpu_count() or 1,
-                          _ptr(s), _ptr(x), _ptr(c), cap, _ptr(hq), _ptr(hr), _ptr(hs))
+    n = lib().oracle_scan_op(_ptr(refs), refs.shape[0], _ptr(queries), nq, refs.shape[1], refs.dtype.itemsize * 8,
+                             k, max_score, int(want), int(threshold or 0), workers or os.cpu_count() or 1,
+                             _ptr(s), _ptr(x), _ptr(c), cap, _ptr(hq), _ptr(hr), _ptr(hs), _SCAN_OPS[op])
     assert n >= 0, "oracle_scan failed"
     top = (s, x, c[:nq]) if k > 0 else None
     hits = None

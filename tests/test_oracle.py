@@ -163,3 +163,21 @@ def test_operator_restatements(rng):
     assert np.array_equal(oracle.np_scores_op(r, q, "andnot").astype(np.int64), pr[:, None] - both)
     with pytest.raises(KeyError):
         oracle.np_scores_op(r, q, "or")
+
+
+@pytest.mark.parametrize("op", ["andnot", "and", "xor"])
+@pytest.mark.parametrize("width", [32, 64])
+def test_scan_operators_match_numpy(rng, op, width):
+    """oracle.scan(op=...) (the C scan bench.py verifies with) == the numpy
+    operator restatement, top-k and threshold."""
+    L = 700
+    nw = -(-L // width)
+    r, _ = rand_words(rng, 3000, nw, width, L)
+    q, _ = rand_words(rng, 7, nw, width, L)
+    exp = oracle.np_scores_op(r, q, op)
+    t = int(np.percentile(exp, 1))
+    (s, x, _), (hq, hr, hs, n) = oracle.scan(r, q, 9, threshold=t, workers=3, op=op)
+    es, ex, _ = oracle.topk_from_matrix(exp, 9)
+    assert np.array_equal(s, es) and np.array_equal(x, ex)
+    eq, er, esc = oracle.threshold_from_matrix(exp, t)
+    assert n == len(eq) and np.array_equal(hq, eq) and np.array_equal(hr, er) and np.array_equal(hs, esc)
