@@ -68,6 +68,14 @@ class PreparedImage:
         _native.check(_native.lib().fastid_db_set_option(self.handle, DB_OPTIONS[name], int(bool(enabled))),
                       "fastid_db_set_option")
 
+    def set_operator(self, op: str) -> None:
+        """The operator of later calls (fastid_db_set_operator); the image is reused."""
+        from . import _native
+
+        _native.check(_native.lib().fastid_db_set_operator(self.handle, _native.operator_code(op)),
+                      "fastid_db_set_operator")
+        self.op = op
+
     @property
     def options(self) -> set:
         from . import _native
@@ -162,6 +170,13 @@ class ChunkedImage:
         if name not in DB_OPTIONS:
             raise ValueError(f"option must be one of {sorted(DB_OPTIONS)}, got {name!r}")
         self._bits = (self._bits | DB_OPTIONS[name]) if enabled else (self._bits & ~DB_OPTIONS[name])
+
+    def set_operator(self, op: str) -> None:
+        """The operator of the chunk handles built from now on."""
+        from . import _native
+
+        _native.operator_code(op)
+        self.op = op
 
     @property
     def options(self) -> set:
@@ -348,6 +363,16 @@ class KnownDatabase:
         variant returns the same result.  No effect without a tensor image."""
         if self.image is not None:
             self.image.set_option(name, enabled)
+
+    def set_operator(self, op: str) -> None:
+        """Switch the bitwise operator ("andnot", "and", "xor") of later searches;
+        the prepared image serves every operator and is not rebuilt."""
+        from . import _native
+
+        _native.operator_code(op)
+        if self.image is not None:
+            self.image.set_operator(op)
+        self.op = op
 
     @property
     def n_profiles(self) -> int:

@@ -177,10 +177,13 @@ def test_db_set_operator_switches_a_prepared_image(rng, form):
     r, q = _case(rng, 7000, 300, L)
     db = KnownDatabase(r, L, formulation=form)
     db.packed_max_queries = db.scan_max_queries = 0  # keep every batch on the image
-    for op in ("andnot", "xor", "and", "xor", "andnot"):
-        _native.check(_native.lib().fastid_db_set_operator(db.image.handle, _native.OPERATORS[op]),
-                      "fastid_db_set_operator")
-        db.op = db.image.op = op
+    for i, op in enumerate(("andnot", "xor", "and", "xor", "andnot")):
+        if i % 2:  # the C ABI directly, and through KnownDatabase.set_operator
+            _native.check(_native.lib().fastid_db_set_operator(db.image.handle, _native.OPERATORS[op]),
+                          "fastid_db_set_operator")
+            db.op = db.image.op = op
+        else:
+            db.set_operator(op)
         exp = oracle.np_scores_op(r, q, op)
         s, x = db.search_words(q, 16)
         es, ex, _ = oracle.topk_from_matrix(exp, 16)
