@@ -190,3 +190,38 @@ def test_db_set_operator_switches_a_prepared_image(rng, form):
         assert np.array_equal(s, es) and np.array_equal(x, ex), op
         full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
         assert np.array_equal(full, exp), op
+
+
+@pytest.mark.parametrize("form", ["tensor_f4", "tensor_i8", "popc"])
+def test_operators_longest_profiles_exact(rng, form):
+    """L = 2^20 loci with AND and XOR: an all-ones known against an all-zero /
+    all-one unknown scores 2^20 / 0 (XOR) and 0 / 2^20 (AND); XOR's signed mxf4
+    accumulator spans [-2^20, 2^20] and stays exact in fp32."""
+    m = fb()
+    from paper_1707_00516_b200.search import KnownDatabase
+
+    L = 1 << 20
+    nw = L // 64
+    r, _ = rand_words(rng, 24, nw, 64, L)
+    q, _ = rand_words(rng, 5, nw, 64, L)
+    r[0] = np.uint64(2**64 - 1)
+    r[1] = 0
+    q[0] = 0
+    q[1] = np.uint64(2**64 - 1)
+    q[2] = r[3]
+    R, Q = m.Panel(tuple(range(24)), r, L), m.Panel(tuple(range(5)), q, L)
+    for op in ("and", "xor"):
+        exp = oracle.np_scores_op(r, q, op, block=4)
+        if op == "xor":
+            assert exp[0, 0] == L and exp[0, 1] == 0 and exp[1, 1] == L and exp[3, 2] == 0
+        else:
+            assert exp[0, 1] == L and exp[0, 0] == 0
+        assert np.array_equal(m.compare_b200(R, Q, formulation=form, op=op).scores, exp), (op, "packed full")
+        es, ex, _ = oracle.topk_from_matrix(exp, 4)
+        res = m.topk(R, Q, 4, formulation=form, op=op)
+        assert np.array_equal(res.scores, es) and np.array_equal(res.index, ex), (op, "packed top-k")
+        db = KnownDatabase(r, L, formulation=form, op=op)
+        full = db.full_device(m.DevicePanel.from_words(q, L)).cpu().numpy().view(np.uint32)
+        assert np.array_equal(full, exp), (op, "image full")
+        s, x = db.search_words(q, 4)
+        assert np.array_equal(s, es) and np.array_equal(x, ex), (op, "image top-k")
