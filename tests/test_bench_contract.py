@@ -66,3 +66,12 @@ def test_spawn_ranks_sets_the_launcher_environment(tmp_path):
     finally:
         bench.__file__ = old
     assert rc == 0
+
+
+def test_reference_arm_has_no_xor():
+    """`--op xor` is a library extension: the reference arm says it is unavailable."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--op", "xor",
+                          "--steps", "1"], capture_output=True, text=True, timeout=120, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    assert d["impl"] == "reference" and "AND-NOT" in d["unavailable"]
