@@ -239,7 +239,7 @@ constexpr int kScanPiece = 8;  // uint4 per row per staging round (128 B)
 constexpr int kScanTile16 = 32 * (kScanPiece + 1);  // one warp's staging tile (uint4), padded rows
 
 template <int MODE, int KP, int QN, bool XOR>
-__global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : 2) popc_scan_kernel(CompareArgs a) {
+__global__ void __launch_bounds__(32 * kScanWarps, QN <= 2 ? 4 : QN <= 4 ? 3 : 2) popc_scan_kernel(CompareArgs a) {
     extern __shared__ __align__(16) uint4 sq[];  // [n_queries][n16] unknown rows (complemented for AND-NOT)
     const int n16 = (int)(a.stride / 16);
     const int nq = (int)a.n_queries;
@@ -525,6 +525,9 @@ int launch_popc(Mode mode, const CompareArgs& a, int* n_parts, cudaStream_t stre
         // 0.535 vs 0.592 ms at 4 (20M x 1024 loci, tools/scan_timing.py); from two
         // unknowns on, the popcount work wants the 4th CTA (4 unknowns: 1.20 vs 1.38 ms)
         if (a.n_queries == 1) parts = std::min(parts, 3 * num_sms());
+        // three or four unknowns: 3 resident CTAs per SM (80 registers), one wave of them
+        // (4 unknowns: 1.12 ms vs 1.20 at 2 per SM in two waves)
+        if (a.n_queries > 2 && a.n_queries <= 4) parts = std::min(parts, 3 * num_sms());
         // FASTID_SCAN_CTAS: grid size of the scan (scheduling only; <= kMaxMergeLists)
         if (const char* e = getenv("FASTID_SCAN_CTAS")) {
             const int v = atoi(e);
