@@ -215,7 +215,7 @@ class ChunkedImage:
 CHUNKED_IMAGE_MIN_QUERIES = 1024
 # Up to this many unknowns an "auto" top-k runs the CUDA-core scan over the packed
 # rows instead of the tensor image (tools/small_batch.py, 20M x 1024 loci, top-16:
-# 1 unknown 0.49 vs 1.61 ms, 2: 0.64 vs 1.57, 4: 1.18 vs 1.57, 8: 2.01 vs 1.59).
+# 1 unknown 0.49 vs 1.61 ms, 2: 0.64 vs 1.57, 4: 1.12 vs 1.57, 8: 2.01 vs 1.59).
 SCAN_MAX_QUERIES = 4
 # Up to this many unknowns (one 128-row group of the single-CTA tensor kernel) an
 # "auto" top-k reads the packed rows, unpacked in shared memory, instead of the
