@@ -17,14 +17,21 @@ from paper_1707_00516_b200.search import KnownDatabase
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 g = torch.Generator(device="cuda").manual_seed(3)
 bad = 0
-for n_r, n_q, L, mode in ((2_000_000, 2048, 1024, "topk"), (1_000_000, 512, 5000, "topk"), (3_000_000, 7, 1024, "topk"),
-                          (500_000, 1000, 2000, "topk"), (300_000, 2048, 1024, "full"), (1_000_000, 300, 3500, "thr")):
+CASES = ((2_000_000, 2048, 1024, "topk", "andnot"), (1_000_000, 512, 5000, "topk", "andnot"),
+         (3_000_000, 7, 1024, "topk", "andnot"), (500_000, 1000, 2000, "topk", "andnot"),
+         (300_000, 2048, 1024, "full", "andnot"), (1_000_000, 300, 3500, "thr", "andnot"),
+         # the CUDA-core scan (1, 2 and 4 unknowns: bulk list updates, 3 CTAs per SM) and
+         # the operators (XOR's signed mxf4 operand, AND)
+         (3_000_000, 1, 1024, "topk", "andnot"), (3_000_000, 2, 1024, "topk", "xor"),
+         (3_000_000, 4, 1024, "topk", "and"), (1_000_000, 2048, 1024, "topk", "xor"),
+         (300_000, 512, 1024, "full", "xor"))
+for n_r, n_q, L, mode, op in CASES:
     nw = -(-L // 64)
     r = torch.randint(-(2**63), 2**63 - 1, (n_r, nw), dtype=torch.int64, device="cuda", generator=g)
     if L % 64:
         r[:, -1] &= ~((1 << (64 - L % 64)) - 1)
     q = r[torch.randint(0, n_r, (n_q,), device="cuda", generator=g)].clone()
-    db = KnownDatabase(m.DevicePanel.from_words(r, L))
+    db = KnownDatabase(m.DevicePanel.from_words(r, L), op=op)
     dq = m.DevicePanel.from_words(q, L)
     qp = m.Panel(tuple(range(n_q)), q.cpu().numpy().view("uint64"), L)
 
@@ -47,7 +54,7 @@ for n_r, n_q, L, mode in ((2_000_000, 2048, 1024, "topk"), (1_000_000, 512, 5000
             n_bad += 1
     torch.cuda.synchronize()
     bad += n_bad
-    print(f"{n_r}x{n_q}x{L} {mode}: {reps} runs in {time.perf_counter() - t0:.1f} s, {n_bad} differing", flush=True)
+    print(f"{n_r}x{n_q}x{L} {mode} {op}: {reps} runs in {time.perf_counter() - t0:.1f} s, {n_bad} differing", flush=True)
     del db, r, q, dq
     torch.cuda.empty_cache()
 print("stress ok" if bad == 0 else f"STRESS FAILED: {bad} differing runs")
