@@ -177,7 +177,10 @@ FASTID_API int fastid_db_create_in(const void* refs, int64_t n_refs, int64_t str
                                    int formulation, void* image, size_t image_bytes, void* stream, fastid_db** out);
 FASTID_API int fastid_db_destroy(fastid_db* db);
 /* The operator (FASTID_OP_*) of the handle's later comparisons (default
- * AND-NOT).  XOR needs each known row's popcount: computed once on first use. */
+ * AND-NOT; fastid_db_create also takes it OR-ed into `formulation`).  The image
+ * serves every operator.  XOR on an i8 image needs each known row's popcount:
+ * computed once on first use (that call synchronises its stream); the mxf4
+ * image needs none (a signed unknown operand, tensor.cu unpack_f4_xor). */
 FASTID_API int fastid_db_set_operator(fastid_db* db, int op);
 FASTID_API int fastid_db_formulation(const fastid_db* db);
 
