@@ -483,7 +483,7 @@ int topk_partials_impl(const void* refs, const void* image, int options, int64_t
                     need);
     // auto, packed rows, a handful of unknowns: the CUDA-core scan reads the packed
     // rows once and beats the tensor kernels there (20M x 1024 loci, top-16:
-    // 1 unknown 0.70 vs 1.52 ms, 4: 1.41 vs 1.54, 8: 2.41 vs 1.55; popc.cu)
+    // 1 unknown 0.49 vs 1.56 ms, 4: 1.12 vs 1.55, 8: 2.00 vs 1.57; popc.cu)
     const int f = ((formulation & ~FASTID_OP_MASK) == FASTID_AUTO && !image && n_queries <= kScanAutoMaxQueries)
                       ? FASTID_POPC
                       : resolve_formulation(formulation, bit_length);
@@ -599,7 +599,8 @@ struct fastid_db {
     int options;      // FASTID_OPT_* bits
     bool owns_image;  // false: the caller's buffer (fastid_db_create_in)
     int op = FASTID_OP_ANDNOT;        // fastid_db_set_operator
-    uint32_t* ref_popc = nullptr;     // per-row popcounts (XOR on the tensor image), owned
+    uint32_t* ref_popc = nullptr;     // per-row popcounts (XOR on the i8 image), owned
+    std::mutex popc_mu;               // guards the lazy ref_popc build (calls may come from several threads)
 };
 
 extern "C" size_t fastid_db_image_bytes(int64_t n_refs, int64_t bit_length, int formulation) {
@@ -673,6 +674,7 @@ namespace {
 int db_ref_popc(fastid_db* db, void* stream, const uint32_t** out) {
     *out = nullptr;
     if (db->op != FASTID_OP_XOR || db->formulation != FASTID_TENSOR_I8 || db->n_refs == 0) return FASTID_OK;
+    std::lock_guard<std::mutex> lock(db->popc_mu);
     if (!db->ref_popc) {
         if (cudaMalloc(&db->ref_popc, (size_t)popcount_entries(db->n_refs) * sizeof(uint32_t)) != cudaSuccess) {
             cudaGetLastError();
