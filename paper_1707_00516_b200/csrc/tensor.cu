@@ -969,12 +969,11 @@ __global__ void __launch_bounds__(Roles<F, IMG>::kThreads, 1)
         // the k-th smallest published minimum is folded into a.bound by every list
         // at tiles 1, 2, 4, ... and then every 256th (SIMT-parallel over lanes)
         const uint32_t hit_bits = MODE == kThreshold ? score_bits<F>(a.threshold) : 0u;
-        // XOR: the MMA counts shared ones (A = the unknown rows as they are) and
-        // popc(r ^ q) = popc(r) + popc(q) - 2 popc(r & q) is formed here, before any
-        // compare, so every mode ranks and stores Hamming distances
-        // (mxf4: the MMA already holds popc(r) - 2 popc(r & q), see unpack_f4_xor, and
-        // popc(q) is stored as fp32 bits: one exact FADD per value; i8: the integer
-        // identity with the known rows' popcounts)
+        // XOR, formed before any compare so every mode ranks and stores Hamming
+        // distances: mxf4 -- the MMA already holds popc(r) - 2 popc(r & q) (signed
+        // unknown operand, unpack_f4_xor) and the epilogue adds popc(q), stored as
+        // fp32 bits (one exact FADD per value); i8 -- the MMA counts shared ones and
+        // popc(r) + popc(q) - 2 popc(r & q) is formed from the known rows' popcounts
         const bool xor_op = a.op == FASTID_OP_XOR;
         const uint32_t pq = xor_op && q_ok ? a.query_popc[q] : 0u;
         uint32_t t_empty_leader[kAccBufs] = {};
