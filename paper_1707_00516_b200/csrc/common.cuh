@@ -165,8 +165,8 @@ struct CompareArgs {
     // operator (FASTID_OP_*) and, for XOR on the tensor kernels (which accumulate
     // popcount(known AND unknown)), the rows' popcounts: xor = pr + pq - 2 * and
     int op;
-    const uint32_t* ref_popc;    // [n_refs]
-    const uint32_t* query_popc;  // [n_queries]
+    const uint32_t* ref_popc;    // XOR on i8: known-row popcounts, popcount_entries(n_refs) long (zero-padded)
+    const uint32_t* query_popc;  // XOR: [n_queries] unknown-row popcounts (fp32 bits for mxf4)
     // threshold
     uint32_t threshold;
     int64_t ref_base;

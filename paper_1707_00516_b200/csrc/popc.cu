@@ -464,7 +464,7 @@ int launch_mode(const CompareArgs& a, int n_slices, cudaStream_t stream) {
     return FASTID_OK;
 }
 
-// One warp per row: the row's popcount (XOR scores on the tensor path).
+// One warp per row: the row's popcount (XOR on the tensor kernels: the unknowns', and the knowns' for i8).
 __global__ void row_popcount_kernel(const uint8_t* __restrict__ rows, int64_t n, int64_t n_out, int64_t stride,
                                     bool as_float, uint32_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
