@@ -162,8 +162,9 @@ struct CompareArgs {
     // CTA-pair kernel: spare pairs and the tiles the regular slices cover (the rest go to spares)
     int n_spare;
     int64_t t_main;
-    // operator (FASTID_OP_*) and, for XOR on the tensor kernels (which accumulate
-    // popcount(known AND unknown)), the rows' popcounts: xor = pr + pq - 2 * and
+    // operator (FASTID_OP_*) and, for XOR on the tensor kernels, the rows' popcounts
+    // (mxf4 accumulates pr - 2 * and with a signed unknown operand and adds pq; i8
+    // accumulates and and forms pr + pq - 2 * and)
     int op;
     const uint32_t* ref_popc;    // XOR on i8: known-row popcounts, popcount_entries(n_refs) long (zero-padded)
     const uint32_t* query_popc;  // XOR: [n_queries] unknown-row popcounts (fp32 bits for mxf4)
