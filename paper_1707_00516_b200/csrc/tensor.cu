@@ -1388,7 +1388,7 @@ inline SparePlan spare_plan(int64_t n_tiles, int64_t groups, int slices, bool di
     const int64_t per = groups / spare;
     // equal tile counts per pair, scaled by FASTID_SPARE_SHARE percent (tuning knob:
     // a spare pair re-reads its tail once per group it serves)
-    static const int share = [] {
+    const int share = [] {  // read per launch (scheduling only: the result is the same)
         const char* e = getenv("FASTID_SPARE_SHARE");
         const int v = e ? atoi(e) : 100;
         return v > 0 && v <= 200 ? v : 100;
